@@ -1,0 +1,234 @@
+"""Pins for the CPU oracle (-m "not gpu").
+
+Every oracle function is checked against something other than itself:
+hand-derived N = 1 / N = 2 values, the Erlang-B closed form, the ordered-hunt
+closed form, brute force (dense LU of pi Q = 0 built by independent code in
+oracle/dense.py), and exact identities of the model.  See DESIGN.md §3 for the
+pin map.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import hqinst
+import oracle
+from oracle import dense
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden", "spec_n2_examples.json")
+
+
+def _examples():
+    with open(GOLD) as f:
+        return {e["name"]: e for e in json.load(f)["examples"]}
+
+
+def _inst(e):
+    return hqinst.from_arrays(e["lam"], e["mu"], e["pref"], name=e["name"])
+
+
+def erlang_b(N, a):
+    """Erlang loss recursion B(0)=1, B(k)=aB(k-1)/(k+aB(k-1))."""
+    B = [1.0]
+    for k in range(1, N + 1):
+        B.append(a * B[-1] / (k + a * B[-1]))
+    return B
+
+
+def truncated_poisson(N, a):
+    w = np.array([a ** n / math.factorial(n) for n in range(N + 1)])
+    return w / w.sum()
+
+
+def layer_mass(pi, N):
+    pc = np.array([bin(m).count("1") for m in range(1 << N)])
+    return np.bincount(pc, weights=pi, minlength=N + 1)
+
+
+# ---------------------------------------------------------------- hand values
+
+@pytest.mark.parametrize("name", ["N2_homogeneous", "N2_heterogeneous", "N1_mm11"])
+def test_hand_examples_pi(name):
+    e = _examples()[name]
+    inst = _inst(e)
+    ref = np.array(e["pi"])
+    lu = dense.stationary(inst.lam, inst.mu, inst.pref)
+    np.testing.assert_allclose(lu, ref, rtol=0, atol=1e-15)
+    r = oracle.solve(inst, tol=1e-15)
+    np.testing.assert_allclose(r["pi"], ref, rtol=0, atol=1e-15)
+    if "layer_mass" in e:
+        np.testing.assert_allclose(layer_mass(r["pi"], inst.N), e["layer_mass"], atol=1e-15)
+    if "layer1_mu" in e:
+        assert abs(r["layer_mu"][1] - e["layer1_mu"]) < 1e-14
+    if "layer1_conditional" in e:
+        p1 = r["pi"][[1, 2]] / r["pi"][[1, 2]].sum()
+        np.testing.assert_allclose(p1, e["layer1_conditional"], atol=1e-15)
+
+
+@pytest.mark.parametrize("name", ["N2_homogeneous", "N2_heterogeneous", "N1_mm11"])
+def test_hand_examples_measures(name):
+    e = _examples()[name]
+    inst = _inst(e)
+    pi = np.array(e["pi"])
+    w, d, loss = oracle.measures(inst, pi)
+    np.testing.assert_allclose(w, e["workload"], atol=1e-15)
+    if "dispatch" in e:
+        np.testing.assert_allclose(d, e["dispatch"], atol=1e-15)
+        assert abs(loss - e["loss"]) < 1e-15
+    w2, d2, loss2 = dense.measures(inst.lam, inst.mu, inst.pref, pi)
+    np.testing.assert_allclose(w2, e["workload"], atol=1e-15)
+
+
+def test_hand_rates_two_atoms():
+    e = _examples()["N2_two_atoms_rates"]
+    inst = _inst(e)
+    for l, ref in e["out_rates"].items():
+        out, lost = oracle.out_rates(inst, int(l))
+        np.testing.assert_allclose(out, ref, atol=1e-15)
+        assert abs(lost - e["lost"][l]) < 1e-15
+    # the dispatch form (Algorithm 3) gives the same numbers seen from the destination
+    for m in range(4):
+        W = oracle.dispatch_rates(inst, m)
+        for i in range(2):
+            if (m >> i) & 1:
+                out, _ = oracle.out_rates(inst, m ^ (1 << i))
+                assert abs(W[i] - out[i]) < 1e-15
+            else:
+                assert W[i] == 0.0
+
+
+# ---------------------------------------------------------------- rates
+
+@pytest.mark.parametrize("L", [None, 3])
+def test_rates_conservation_and_dense_agreement(L):
+    inst = hqinst.generate(7, 15, seed=11, rho=0.6, L=L)
+    Q = dense.generator_matrix(inst.lam, inst.mu, inst.pref)
+    Lam = inst.lam.sum()
+    for l in range(1 << inst.N):
+        out, lost = oracle.out_rates(inst, l)
+        assert abs(out.sum() + lost - Lam) < 1e-12          # every call goes somewhere or is lost
+        for i in range(inst.N):
+            if not (l >> i) & 1:
+                assert abs(Q[l, l | (1 << i)] - out[i]) < 1e-14   # independent construction
+        if L is None and l != (1 << inst.N) - 1:
+            assert lost == 0.0                                     # full lists: lambda_m = lambda
+    for m in range(1 << inst.N):
+        W = oracle.dispatch_rates(inst, m)
+        for i in range(inst.N):
+            if (m >> i) & 1:
+                assert abs(W[i] - Q[m ^ (1 << i), m]) < 1e-14
+
+
+# ---------------------------------------------------------------- brute force
+
+_VARIANTS = [
+    dict(N=8, J=20, clustered=False, L=None, mu_lo=0.5, mu_hi=1.5),
+    dict(N=9, J=30, clustered=True, L=None, mu_lo=0.3, mu_hi=2.0),
+    dict(N=9, J=40, clustered=False, L=4, mu_lo=0.5, mu_hi=1.5),
+    dict(N=10, J=20, clustered=False, L=None, mu_lo=0.5, mu_hi=1.5),
+]
+
+
+@pytest.mark.parametrize("var", range(len(_VARIANTS)))
+@pytest.mark.parametrize("rho", [0.1, 0.3, 0.6, 0.9])
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_alg1_matches_dense_lu(var, rho, seed):
+    v = _VARIANTS[var]
+    inst = hqinst.generate(v["N"], v["J"], seed=seed, rho=rho, mu_lo=v["mu_lo"], mu_hi=v["mu_hi"],
+                           clustered=v["clustered"], L=v["L"])
+    lu = dense.stationary(inst.lam, inst.mu, inst.pref)
+    r = oracle.solve(inst, tol=1e-14, max_iter=3000)
+    assert r["status"] == 0, r
+    assert np.abs(r["pi"] - lu).sum() <= 1e-11
+    assert np.abs(r["pi"] - lu).max() <= 1e-13
+    assert abs(r["pi"].sum() - 1.0) <= 1e-13
+    # measures: C oracle vs the independent enumeration in dense.py
+    w, d, loss = oracle.measures(inst, r["pi"])
+    w2, d2, loss2 = dense.measures(inst.lam, inst.mu, inst.pref, lu)
+    assert np.abs(w - w2).max() < 1e-12 and np.abs(d - d2).max() < 1e-12 and abs(loss - loss2) < 1e-12
+
+
+def test_residual_matches_dense_definition():
+    inst = hqinst.generate(8, 12, seed=5, rho=0.5, L=5)
+    rng = np.random.default_rng(0)
+    pi = rng.random(1 << inst.N)
+    pi /= pi.sum()
+    Q = dense.generator_matrix(inst.lam, inst.mu, inst.pref)
+    ref = np.abs(pi @ Q).sum() / (pi * -np.diag(Q)).sum()
+    assert abs(oracle.residual(inst, pi) - ref) < 1e-14
+    # per-state balance gives the same numbers
+    states = np.arange(1 << inst.N, dtype=np.uint64)
+    nbr = np.stack([pi] + [pi[np.arange(1 << inst.N) ^ (1 << i)] for i in range(inst.N)], axis=1)
+    o, i_ = oracle.state_balance(inst, states, nbr)
+    assert abs(np.abs(o - i_).sum() / o.sum() - ref) < 1e-14
+
+
+# ---------------------------------------------------------------- closed forms
+
+@pytest.mark.parametrize("cfg,N", [(1, 10), (2, 14), (3, 16)])
+def test_erlang_layer_masses_homogeneous(cfg, N):
+    """Homogeneous nu with full lists: the busy count is M/M/N/N, so the layer
+    masses are the truncated Poisson (Erlang loss) law, whatever the lists."""
+    inst = hqinst.homogeneous_copy(hqinst.config_instance(cfg, N=N, J=40))
+    r = oracle.solve(inst, tol=1e-14, max_iter=4000)
+    a = inst.lam.sum() / 1.0
+    np.testing.assert_allclose(layer_mass(r["pi"], N), truncated_poisson(N, a), rtol=0, atol=1e-13)
+    if N <= 10:
+        lu = dense.stationary(inst.lam, inst.mu, inst.pref)
+        np.testing.assert_allclose(layer_mass(lu, N), truncated_poisson(N, a), rtol=0, atol=1e-14)
+
+
+@pytest.mark.parametrize("N,rho", [(7, 0.47), (12, 0.6), (15, 0.9)])
+def test_ordered_hunt_closed_form(N, rho):
+    """Ordered hunt (every atom, same list), nu = 1: the k-th unit of the order
+    carries a (B(k-1,a) - B(k,a)) and the loss is B(N,a)."""
+    order = np.random.default_rng(N).permutation(N).astype(np.int32)
+    inst = hqinst.ordered_hunt(N, rho, J=3, order=order)
+    a = inst.lam.sum()
+    B = erlang_b(N, a)
+    r = oracle.solve(inst, tol=1e-14, max_iter=4000)
+    w, d, loss = oracle.measures(inst, r["pi"])
+    ref = np.zeros(N)
+    for k, u in enumerate(order, start=1):
+        ref[u] = a * (B[k - 1] - B[k])
+    np.testing.assert_allclose(w, ref, rtol=0, atol=1e-12)
+    assert abs(loss - B[N]) < 1e-13
+    if N <= 10:
+        lu = dense.stationary(inst.lam, inst.mu, inst.pref)
+        w2, _, loss2 = dense.measures(inst.lam, inst.mu, inst.pref, lu)
+        np.testing.assert_allclose(w2, ref, rtol=0, atol=1e-14)
+
+
+# ---------------------------------------------------------------- identities
+
+@pytest.mark.parametrize("L", [None, 4])
+def test_flow_identities(L):
+    inst = hqinst.generate(11, 60, seed=9, rho=0.7, L=L)
+    r = oracle.solve(inst, tol=1e-14, max_iter=3000)
+    pi = r["pi"]
+    N = inst.N
+    w, d, loss = oracle.measures(inst, pi)
+    Lam = inst.lam.sum()
+    assert abs(d.sum() - 1.0) < 1e-12                                   # every served call dispatches one unit
+    np.testing.assert_allclose(inst.mu * w, Lam * (1 - loss) * d.sum(axis=0), rtol=0, atol=1e-12)  # unit flow
+    # layer cut balance: P(n-1) lambda(n-1) = P(n) mu(n)  (birth-death structure)
+    P = layer_mass(pi, N)
+    ll, lm = r["layer_lambda"], r["layer_mu"]
+    for n in range(1, N + 1):
+        assert abs(P[n - 1] * ll[n - 1] - P[n] * lm[n]) < 1e-13
+    assert (pi >= 0).all()
+    if L is None:
+        assert abs(loss - pi[-1]) < 1e-15   # full lists: lost iff all busy
+
+
+def test_alg1_residual_decreases_geometrically():
+    """Theorem 1: the iterates converge geometrically; the
+    trace of r(pi) falls by a roughly constant factor per sweep."""
+    inst = hqinst.config_instance(1)
+    r = oracle.solve(inst, tol=1e-13, trace=True)
+    tr = r["trace"]
+    ratios = tr[11:] / tr[10:-1]
+    assert (ratios < 1.0).all()
+    assert 0.3 < np.median(ratios) < 0.95
