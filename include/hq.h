@@ -1,0 +1,145 @@
+/*
+ * hq.h -- C-ABI of the B200-native steady-state solver for the spatial
+ * hypercube queueing model with heterogeneous service rates
+ * (arXiv 2603.03019; PAPER.md = the paper's text).
+ *
+ * The library (libhq.so, built from paper_2603_03019_b200/csrc) runs every
+ * step of the solve in hand-written sm_100a CUDA kernels.  There is no CPU
+ * fallback: on a machine without a usable CUDA device every compute call
+ * returns HQ_E_CUDA.
+ *
+ * Model.  N units, J demand atoms.  State m in [0, 2^N):
+ * bit u of m is 1 iff unit u (0-based) is busy, i.e. the paper's index
+ * y(B_m) with paper unit i = u + 1.  An arrival at atom j
+ * (rate lambda[j] = lambda * f_j) is served by the first free unit of the
+ * atom's preference list (Eq. tran_rates); if every unit of
+ * the list is busy the call is lost (C = 0).  A busy
+ * unit u completes service at rate mu[u] (the paper's nu_i).
+ *
+ * Thread safety: calls on different handles may run concurrently; calls on
+ * one handle must be serialised by the caller.
+ */
+#ifndef HQ_H
+#define HQ_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct hq_problem *hq_handle;
+
+typedef enum {
+    HQ_OK = 0,
+    HQ_NOT_CONVERGED = 1, /* warning: max_iter reached; outputs hold the last iterate */
+    HQ_E_INVAL = -1,      /* invalid argument; see hq_error_string                     */
+    HQ_E_NOMEM = -2,      /* device memory for the working set could not be allocated  */
+    HQ_E_CUDA = -3,       /* CUDA runtime / launch error (or no device)                */
+    HQ_E_NUMERIC = -4,    /* NaN/Inf or a non-positive normaliser in the iteration     */
+    HQ_E_ORDER = -5       /* hq_measures before a successful hq_solve on this handle  */
+} hq_status;
+
+/*
+ * hq_create -- validate an instance and build its device-side tables
+ * (preference trie for on-the-fly upward rates, service rates).
+ *
+ *   N       number of units, 1 <= N <= 31 (2^31 states, 17.2 GB fp64 pi).
+ *   J       number of demand atoms, J >= 1.
+ *   lambda  [J] host, per-atom arrival rates lambda_j = lambda * f_j
+ *           (PAPER.md:76, 96-97); each finite and >= 0, sum > 0.
+ *   mu      [N] host, per-unit service rates (the paper's nu_i,
+ *           PAPER.md:99); each finite and > 0.
+ *   pref    [J][N] host, row-major int32: pref[j*N + h] is the 0-based id of
+ *           the (h+1)-th preferred unit of atom j (the paper's zeta_j(h+1),
+ *           PAPER.md:93).  A row may end early with -1 padding (truncated
+ *           list: the call is lost when all listed units are busy).  Entries
+ *           must be in [0, N), distinct within a row, no entry after a -1,
+ *           rows non-empty.  Every unit must appear in the list of some atom
+ *           with lambda_j > 0 (otherwise the chain is reducible and the
+ *           stationary distribution is not unique).
+ *   out     receives the handle.
+ *
+ * Ownership: the input arrays are copied; the caller may free them on
+ * return.  The handle owns all device tables and scratch (allocated on the
+ * current device at the first hq_solve), released by hq_destroy.
+ * Errors: HQ_E_INVAL (message via hq_error_string(NULL)), HQ_E_CUDA.
+ */
+hq_status hq_create(int N, int J, const double *lambda, const double *mu, const int32_t *pref, hq_handle *out);
+
+/*
+ * hq_solve -- the layer-ordered conditional-probability iteration
+ * (Algorithm 1, Eqs. updateHeter / lambdaHeter / muHeter,
+ * PAPER.md:313-320) to a relative balance residual <= tol, then the
+ * assembly P{B_m} = p(w(B_m)) p_{w(B_m)}(B_m) (Proposition 1, PAPER.md:224,
+ * Eq. bnd_stationary).
+ *
+ *   tol       target of the relative L1 global-balance residual
+ *             r(pi) = sum_m |pi(m)(lambda_m + mu_m) - inflow(m)| /
+ *                     sum_m pi(m)(lambda_m + mu_m)        (Eq. balance_eq_heter,
+ *             PAPER.md:161; reading R3).  tol <= 0 runs exactly
+ *             max_iter sweeps.
+ *   max_iter  maximum number of sweeps (each sweep updates layers 1..N-1
+ *             once, i.e. 2^N - 2 states).
+ *   pi        [2^N] DEVICE fp64, caller-owned (e.g. a torch.float64 CUDA
+ *             tensor); on return pi[m] = P{B_m} at natural index m.
+ *   cuda_stream  cudaStream_t to run on (NULL = legacy default stream).
+ *   iters_out    host: sweeps performed.
+ *   residual_out host: the true r(pi) of the returned pi (not a proxy).
+ *
+ * The call synchronises cuda_stream before returning.
+ * Returns HQ_OK, HQ_NOT_CONVERGED (pi, iters, residual hold the last
+ * iterate), HQ_E_INVAL, HQ_E_NOMEM, HQ_E_CUDA or HQ_E_NUMERIC.
+ */
+hq_status hq_solve(hq_handle h, double tol, int max_iter, double *pi, void *cuda_stream, int *iters_out,
+                   double *residual_out);
+
+/*
+ * hq_measures -- performance measures of a stationary distribution pi
+ * (device, natural index, normally the output of hq_solve on this handle).
+ *
+ *   workload  [N] DEVICE fp64: rho_i = P(unit i busy) = sum_{m: bit i} pi(m)
+ *             ("Unit Utilization").
+ *   dispatch  [J*N] DEVICE fp64, row-major [j][i]: the fraction of served
+ *             calls that come from atom j and are served by unit i,
+ *             rho_ij = f_j sum_{m in S_ij} pi(m) / (1 - loss), S_ij = states in
+ *             which i is atom j's first free unit (PAPER.md:787-789,
+ *             1759-1761); sum_ij rho_ij = 1.  Zero for units not in the list.
+ *   loss      host scalar: fraction of arrivals lost,
+ *             sum_j f_j P(every unit of list j busy) (= P{all busy} for full
+ *             lists, the paper's Pi).
+ *   cuda_stream  as in hq_solve; the call synchronises it before returning.
+ * Returns HQ_OK, HQ_E_ORDER (no successful hq_solve yet), HQ_E_INVAL,
+ * HQ_E_NOMEM, HQ_E_CUDA.  The size of pi cannot be checked: it is the
+ * caller's contract.
+ */
+hq_status hq_measures(hq_handle h, const double *pi, double *workload, double *dispatch, double *loss,
+                      void *cuda_stream);
+
+/* Release every device and host resource of h (NULL is a no-op). */
+void hq_destroy(hq_handle h);
+
+/* Last error text for h; h == NULL returns the last hq_create error. */
+const char *hq_error_string(hq_handle h);
+
+/*
+ * Introspection for tests and the benchmark (not part of the paper's
+ * problem statement).  hq_stats fills a host array of HQ_STATS_LEN doubles
+ * describing the last hq_solve:
+ *   [0] sweeps, [1] half-sweeps, [2] state updates (sum over updated layers
+ *   of C(N,n)), [3] kernel launches, [4] true-residual evaluations,
+ *   [5] trie nodes, [6] sum(pi) - 1, [7] solve time in ms (CUDA events),
+ *   [8] time in the sweep kernels in ms (CUDA events), [9] sweep-kernel
+ *   launches, [10] residual-kernel time in ms.
+ */
+#define HQ_STATS_LEN 16
+hq_status hq_stats(hq_handle h, double *out);
+
+/* Library build string (compiler, arch, git-independent version tag). */
+const char *hq_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HQ_H */

@@ -1,0 +1,60 @@
+"""Write oracle fixtures for GPU parity at sizes too slow to re-run the oracle
+in every GPU test session.  Calls only ``oracle`` and ``hqinst``.
+
+  python tests/golden/make_oracle_fixtures.py cfg3
+
+writes tests/golden/oracle_cfg3.npz with: the instance hash, the oracle's
+sweeps and residual, the layer masses, the measures, and pi at a seeded
+sample of states (every state of the three lowest and three highest layers,
+plus uniform random states).
+"""
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+
+import hqinst  # noqa: E402
+import oracle  # noqa: E402
+
+
+def sample_states(N, nrand=6000, seed=123):
+    rng = np.random.default_rng(seed)
+    S = 1 << N
+    edge = [m for m in range(S) if bin(m).count("1") in (0, 1, 2, N - 2, N - 1, N)] if N <= 26 else []
+    rnd = rng.integers(0, S, size=nrand)
+    return np.unique(np.concatenate([np.array(edge, dtype=np.int64), rnd.astype(np.int64)]))
+
+
+def main(which):
+    if which == "cfg3":
+        inst = hqinst.config_instance(3)
+    else:
+        raise SystemExit("unknown fixture " + which)
+    t = time.time()
+    r = oracle.solve(inst, tol=1e-13, max_iter=3000)
+    dt = time.time() - t
+    pi = r["pi"]
+    N = inst.N
+    pc = np.array([bin(m).count("1") for m in range(1 << N)], dtype=np.int64) if N <= 20 else None
+    if pc is None:
+        # popcount by bytes
+        idx = np.arange(1 << N, dtype=np.uint32)
+        pc = np.zeros(1 << N, dtype=np.int64)
+        for sh in range(0, 32, 8):
+            pc += np.array([bin(b).count("1") for b in range(256)], dtype=np.int64)[(idx >> sh) & 0xFF]
+    masses = np.bincount(pc, weights=pi, minlength=N + 1)
+    w, d, loss = oracle.measures(inst, pi)
+    st = sample_states(N)
+    out = os.path.join(HERE, f"oracle_{which}.npz")
+    np.savez_compressed(out, sha256=inst.sha256(), iters=r["iters"], residual=r["residual"], status=r["status"],
+                        masses=masses, workload=w, dispatch=d, loss=loss, states=st, pi_states=pi[st],
+                        oracle_seconds=dt, oracle_threads=oracle.num_threads(), tol=1e-13)
+    print(f"wrote {out}: iters={r['iters']} residual={r['residual']:.3e} time={dt:.1f}s threads={oracle.num_threads()}")
+
+
+if __name__ == "__main__":
+    main(sys.argv[1] if len(sys.argv) > 1 else "cfg3")
