@@ -1,0 +1,354 @@
+#!/usr/bin/env python
+"""Benchmark: state-updates/s and time-to-1e-13 residual (fp64) on one B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
+
+A "step" is one pass of the whole hot path on the resident instance: hq_solve
+from the uniform initial iterate to relative residual <= 1e-13 (Algorithm 1
+sweeps, verification residual, assembly of pi) followed by hq_measures.
+value = state updates (sum over updated layers of C(N,n), i.e. 2^N - 2 per
+sweep) / device time of the K steps (CUDA events, max over ranks).
+
+Multi-GPU: the solve does not shard ("replicas only"): under
+torchrun every rank solves its own replica and value is the sum over ranks /
+the max time ("scaling": "weak").
+
+--impl reference times the CPU oracle (oracle/, the test-infrastructure
+reference implementation written from the paper) on a bounded sample of the
+same workload, on rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "state-updates/sec and time-to-1e-13 residual (fp64) vs HBM roofline, 1 B200"
+UNIT = "state-updates/s"
+BYTES_PER_UPDATE = 32  # read p_{n-1}, p_{n+1} (16 B amortised), read + write p_n (16 B)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=3, help="BASELINE.json config 1..5 (default 3: N=24)")
+    ap.add_argument("--rho", type=float, default=None)
+    ap.add_argument("--tol", type=float, default=1e-13)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-clocks", action="store_true")
+    return ap.parse_args()
+
+
+def workload_desc(inst, cfg):
+    return {"workload": f"cfg{cfg}: {inst.name} N={inst.N} J={inst.J} rho={inst.rho:g} "
+                        f"{'top-8 truncated' if (inst.pref < 0).any() else 'full'} lists, 2^{inst.N} states",
+            "N": inst.N, "J": inst.J, "rho": inst.rho, "seed": inst.seed, "tol": None,
+            "instance_sha256": inst.sha256()[:16]}
+
+
+# ------------------------------------------------------------------ clocks
+
+class Clocks:
+    def __init__(self, enabled=True, index=0):
+        self.enabled = enabled
+        self.proc = None
+        self.path = None
+        self.index = index
+
+    def start(self):
+        if not self.enabled:
+            return
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        with open(self.path) as f:
+            for line in f:
+                p = [x.strip() for x in line.split(",")]
+                if len(p) >= 9:
+                    rows.append(p)
+        os.unlink(self.path)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        smax = max(float(r[2]) for r in rows if r[2].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": reasons,
+                "samples": len(rows), "power_w_max": max(float(r[3]) for r in rows)}
+
+
+# ------------------------------------------------------------------ peaks / profiles
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy test)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(cfg):
+    """dram bytes (read + write) per sweep (gather + finalize launch pair) from the
+    committed ncu --set full summary, if one exists for this config."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    e = d.get(f"cfg{cfg}")
+    return None if e is None else e.get("dram_bytes_per_state_update")
+
+
+# ------------------------------------------------------------------ reference arm (CPU oracle)
+
+def oracle_sample(inst, sweeps=3):
+    """Time `sweeps` oracle sweeps on this host, excluding the one-off rate
+    table build: t(1 + sweeps) - t(1)."""
+    import oracle
+
+    t0 = time.perf_counter()
+    oracle.solve(inst, tol=0.0, max_iter=1)
+    t1 = time.perf_counter()
+    oracle.solve(inst, tol=0.0, max_iter=1 + sweeps)
+    t2 = time.perf_counter()
+    dt = (t2 - t1) - (t1 - t0)
+    updates = ((1 << inst.N) - 2) * sweeps
+    return updates / dt, dt, oracle.num_threads()
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    import hqinst
+
+    inst = hqinst.config_instance(args.config, rho=args.rho)
+    sweeps = 1 if inst.N >= 26 else 2
+    for _ in range(args.warmup if inst.N <= 20 else 0):
+        oracle_sample(inst, 1)
+    vals = []
+    tt = 0.0
+    for _ in range(args.steps):
+        v, dt, cores = oracle_sample(inst, sweeps)
+        vals.append(v)
+        tt += dt
+    value = statistics.median(vals)
+    sample = f"{sweeps} Algorithm-1 sweeps (+ per-sweep residual) of cfg{args.config} per step, rate-table build excluded"
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * tt / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_desc(inst, args.config),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ our arm
+
+def run_ours(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+
+    import hqinst
+    from paper_2603_03019_b200 import hq
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+    inst = hqinst.config_instance(args.config, rho=args.rho)
+    solver = hq.Solver.from_instance(inst)
+    pi = torch.empty(1 << inst.N, dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        r = solver.solve(tol=args.tol, max_iter=100000, pi=pi, stream=stream)
+        solver.measures(pi, stream=stream)
+        if r["status"] != 0:
+            raise RuntimeError(f"solve did not converge: {r}")
+        return r
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clocks = Clocks(enabled=(not args.no_clocks) and rank == 0, index=local_rank)
+    clocks.start()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    e0.record(stream)
+    updates = 0.0
+    sweep_ms = 0.0
+    sweep_launches = 0.0
+    launches = 0.0
+    iters = []
+    res = []
+    solve_ms = []
+    for _ in range(args.steps):
+        r = step()
+        st = solver.stats()
+        updates += st["state_updates"]
+        sweep_ms += st["sweep_ms"]
+        sweep_launches += st["sweep_launches"]
+        launches += st["launches"] + 3 + inst.N   # + measures: copy, N zeta passes, measures kernel
+        iters.append(r["iters"])
+        res.append(r["residual"])
+        solve_ms.append(st["solve_ms"])
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    ck = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    if dist:
+        t = torch.tensor([ms, updates], dtype=torch.float64, device=dev)
+        mx = t.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = t.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        ms_max, updates_tot = float(mx[0]), float(sm[1])
+    else:
+        ms_max, updates_tot = ms, updates
+
+    # ---- e2e: through the C-ABI with host buffers, h2d + d2h inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        lam_h = torch.from_numpy(inst.lam.copy()).pin_memory()
+        mu_h = torch.from_numpy(inst.mu.copy()).pin_memory()
+        pref_h = torch.from_numpy(inst.pref.copy()).pin_memory()
+        pi_h = torch.empty(1 << inst.N, dtype=torch.float64).pin_memory()
+        w_h = torch.empty(inst.N, dtype=torch.float64).pin_memory()
+        d_h = torch.empty(inst.J * inst.N, dtype=torch.float64).pin_memory()
+        e2e_steps = max(1, min(args.steps, 3))
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        e2e_updates = 0.0
+        for _ in range(e2e_steps):
+            s2 = hq.Solver(lam_h.numpy(), mu_h.numpy(), pref_h.numpy())
+            r2 = s2.solve(tol=args.tol, max_iter=100000, pi=pi, stream=stream)
+            m2 = s2.measures(pi, stream=stream)
+            pi_h.copy_(pi, non_blocking=True)
+            w_h.copy_(m2["workload"], non_blocking=True)
+            d_h.copy_(m2["dispatch"].reshape(-1), non_blocking=True)
+            torch.cuda.synchronize()
+            e2e_updates += s2.stats()["state_updates"]
+            s2.close()
+        t_e2e = time.perf_counter() - t0
+        if dist:
+            t = torch.tensor([t_e2e, e2e_updates], dtype=torch.float64, device=dev)
+            mx = t.clone()
+            dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+            sm = t.clone()
+            dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+            t_e2e, e2e_updates = float(mx[0]), float(sm[1])
+        h2d = inst.lam.nbytes + inst.mu.nbytes + inst.pref.nbytes
+        d2h = (8 << inst.N) + 8 * inst.N + 8 * inst.J * inst.N + 8 + 8
+        e2e = {"value": e2e_updates / t_e2e, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": 1000.0 * t_e2e / e2e_steps,
+               "timing": "host wall clock around create + solve + measures + d2h + sync, max over ranks"}
+
+    if rank != 0:
+        solver.close()
+        return 0
+
+    peak, peak_src = measured_peaks()
+    per_update_ms = sweep_ms / max(updates, 1.0)
+    achieved = BYTES_PER_UPDATE * updates / (sweep_ms * 1e-3) / 1e9 if sweep_ms > 0 else None
+    traffic = ncu_traffic(args.config)
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": (achieved / peak) if achieved else None,
+                "traffic": traffic, "traffic_unit": "dram bytes per state update (ncu --set full)" if traffic else None,
+                "kernel": "sweep = k_gather + k_layer_reduce + k_finalize per half-sweep (CUDA events on the solve stream)",
+                "algorithmic_bytes_per_state_update": BYTES_PER_UPDATE, "peak_source": peak_src,
+                "sweep_ms_per_step": sweep_ms / args.steps, "sweep_share_of_step": sweep_ms / ms if ms else None}
+    line = {"metric": METRIC, "value": updates_tot / (ms_max * 1e-3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded EMS-shaped instance, hqinst)",
+            "config": dict(workload_desc(inst, args.config), tol=args.tol,
+                           l2="working set (pi + p + (a,b) scratch) = %.0f MB vs 126 MB L2" % (3 * 8 * (1 << inst.N) / 2 ** 20),
+                           parallelism="replicas" if world > 1 else "single GPU"),
+            "time_to_tol_ms": statistics.median(solve_ms), "sweeps": statistics.median(iters),
+            "residual": max(res), "roofline": roofline, "gpu_launches": int(launches),
+            "e2e": e2e}
+    if ck:
+        line["clocks"] = ck
+    if not args.no_cpu_baseline and world == 1:
+        try:
+            v, dt, cores = oracle_sample(inst, 1 if inst.N >= 26 else 2)
+            line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+                                    "sample": f"{1 if inst.N >= 26 else 2} Algorithm-1 sweeps of cfg{args.config} "
+                                              f"(+ per-sweep residual), rate-table build excluded, {dt:.1f} s"}
+        except Exception as ex:  # the oracle is a reported baseline, never the product
+            line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": None, "kind": "oracle",
+                                    "sample": f"failed: {ex}"}
+    print(json.dumps(line), flush=True)
+    solver.close()
+    return 0
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        return run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    sys.exit(main())

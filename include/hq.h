@@ -130,10 +130,18 @@ const char *hq_error_string(hq_handle h);
  *   of C(N,n)), [3] kernel launches, [4] true-residual evaluations,
  *   [5] trie nodes, [6] sum(pi) - 1, [7] solve time in ms (CUDA events),
  *   [8] time in the sweep kernels in ms (CUDA events), [9] sweep-kernel
- *   launches, [10] residual-kernel time in ms.
+ *   launches, [10] residual-kernel time in ms, [11] one-off per-instance
+ *   precompute time in ms (rate programs, scatter weights), [12] bytes of
+ *   rate programs, [13] code path (1: N < 8 two-pass, 2: tiled single pass).
  */
 #define HQ_STATS_LEN 16
 hq_status hq_stats(hq_handle h, double *out);
+
+/* Copy an internal device array to host memory (tests and debugging only):
+ * which = 0 scalar block, 1 conditional probabilities, 2 scatter weights,
+ * 3 rate programs, 4 program offsets, 5 tile order, 6 internal->ABI unit map.
+ * Returns HQ_E_ORDER if the array does not exist yet. */
+hq_status hq_debug_copy(hq_handle h, int which, void *host, size_t bytes);
 
 /* Library build string (compiler, arch, git-independent version tag). */
 const char *hq_version(void);

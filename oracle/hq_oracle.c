@@ -177,6 +177,7 @@ typedef struct {
     const inst_t *I;
     double *Wtab;    /* [2^N * N] cached Algorithm 3 output, or NULL */
     double *lamtab;  /* [2^N] lambda_m, or NULL */
+    double *mutab;   /* [2^N] mu_m, or NULL */
 } rates_t;
 
 static void state_W(const rates_t *R, uint64_t m, double *W) {
@@ -186,6 +187,10 @@ static void state_W(const rates_t *R, uint64_t m, double *W) {
 
 static double state_lambda(const rates_t *R, uint64_t m) {
     return R->lamtab ? R->lamtab[m] : lambda_m(R->I, m);
+}
+
+static double state_mu(const rates_t *R, uint64_t m) {
+    return R->mutab ? R->mutab[m] : mu_m(R->I, m);
 }
 
 /* ---------------------------------------------------------------------- */
@@ -223,7 +228,7 @@ static double residual(const rates_t *R, const double *pi) {
             uint64_t m = (uint64_t)mm;
             state_W(R, m, W);
             double lm = state_lambda(R, m);
-            double out = pi[m] * (lm + mu_m(I, m));
+            double out = pi[m] * (lm + state_mu(R, m));
             double in = 0.0;
             for (int i = 0; i < N; i++) {
                 uint64_t l = m ^ (1ULL << i);
@@ -269,16 +274,20 @@ int oracle_solve(int N, int J, const double *lam, const double *mu, const int32_
     if (N < 1 || N > 31 || J < 1) return ORACLE_E_INVAL;
     inst_t I = {N, J, lam, mu, pref};
     uint64_t S = 1ULL << N;
-    rates_t R = {&I, NULL, NULL};
+    rates_t R = {&I, NULL, NULL, NULL};
+    /* per-state lambda_m and mu_m are cached (same arithmetic, computed once) */
+    R.lamtab = (double *)malloc(sizeof(double) * S);
+    R.mutab = (double *)malloc(sizeof(double) * S);
+    if (!R.lamtab || !R.mutab) { free(R.lamtab); free(R.mutab); return ORACLE_E_NOMEM; }
     if (use_table) {
         R.Wtab = (double *)malloc(sizeof(double) * S * (uint64_t)N);
-        R.lamtab = (double *)malloc(sizeof(double) * S);
-        if (!R.Wtab || !R.lamtab) { free(R.Wtab); free(R.lamtab); return ORACLE_E_NOMEM; }
+        if (!R.Wtab) { free(R.lamtab); free(R.mutab); return ORACLE_E_NOMEM; }
+    }
 #pragma omp parallel for schedule(static)
-        for (int64_t m = 0; m < (int64_t)S; m++) {
-            dispatch_rates(&I, (uint64_t)m, R.Wtab + (uint64_t)m * N);
-            R.lamtab[m] = lambda_m(&I, (uint64_t)m);
-        }
+    for (int64_t m = 0; m < (int64_t)S; m++) {
+        if (R.Wtab) dispatch_rates(&I, (uint64_t)m, R.Wtab + (uint64_t)m * N);
+        R.lamtab[m] = lambda_m(&I, (uint64_t)m);
+        R.mutab[m] = mu_m(&I, (uint64_t)m);
     }
 
     double *p = (double *)malloc(sizeof(double) * S);   /* p_n(B_m) at natural index m */
@@ -305,7 +314,7 @@ int oracle_solve(int N, int J, const double *lam, const double *mu, const int32_
         for (uint64_t t = 0; t < cnt[n]; t++) {
             uint64_t m = lay[n][t];
             sl += p[m] * state_lambda(&R, m);
-            sm += p[m] * mu_m(&I, m);
+            sm += p[m] * state_mu(&R, m);
         }
         lam_n[n] = sl;   /* Eq. lambdaHeter; lambda(N) = 0 for C = 0 full lists */
         mu_n[n] = sm;    /* Eq. muHeter; mu(0) = 0 */
@@ -333,7 +342,7 @@ int oracle_solve(int N, int J, const double *lam, const double *mu, const int32_
                         if ((m >> i) & 1) up_in += p[l] * W[i];   /* l in C_{n-1}, lambda_lm = W[i] */
                         else down_in += p[l] * mu[i];            /* l in C_{n+1}^m, mu_lm = nu_i    */
                     }
-                    double den = state_lambda(&R, m) + mu_m(&I, m);
+                    double den = state_lambda(&R, m) + state_mu(&R, m);
                     a[m] = up_in / (lam_prev * den);
                     b[m] = ratio * down_in / den;
                 }
@@ -342,7 +351,7 @@ int oracle_solve(int N, int J, const double *lam, const double *mu, const int32_
             double sma = 0.0, smb = 0.0, amax = 0.0;
             for (uint64_t t = 0; t < c; t++) {
                 uint64_t m = L[t];
-                double mm = mu_m(&I, m);
+                double mm = state_mu(&R, m);
                 sma += mm * a[m];
                 smb += mm * b[m];
                 if (a[m] > amax) amax = a[m];
@@ -368,7 +377,7 @@ int oracle_solve(int N, int J, const double *lam, const double *mu, const int32_
                 uint64_t m = L[t];
                 p[m] /= sp;
                 sl += p[m] * state_lambda(&R, m);
-                sm += p[m] * mu_m(&I, m);
+                sm += p[m] * state_mu(&R, m);
             }
             lam_n[n] = sl;   /* Eq. lambdaHeter */
             mu_n[n] = sm;    /* Eq. muHeter     */
@@ -389,13 +398,13 @@ int oracle_solve(int N, int J, const double *lam, const double *mu, const int32_
 
     for (int n = 0; n <= N; n++) free(lay[n]);
     free(lay); free(cnt); free(p); free(a); free(b); free(lam_n); free(mu_n); free(pn);
-    free(R.Wtab); free(R.lamtab);
+    free(R.Wtab); free(R.lamtab); free(R.mutab);
     return status;
 }
 
 double oracle_residual(int N, int J, const double *lam, const double *mu, const int32_t *pref, const double *pi) {
     inst_t I = {N, J, lam, mu, pref};
-    rates_t R = {&I, NULL, NULL};
+    rates_t R = {&I, NULL, NULL, NULL};
     return residual(&R, pi);
 }
 

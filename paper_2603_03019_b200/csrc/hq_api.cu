@@ -24,6 +24,7 @@
 
 #include "../../include/hq.h"
 #include "hq_internal.h"
+#include "hq_v2.h"
 
 namespace hqk_launch {
 cudaError_t gather(const KArgs &k, int grid, cudaStream_t s);
@@ -37,6 +38,7 @@ cudaError_t zeta(int N, double *g, int grid, cudaStream_t s);
 cudaError_t measures(int N, int J, const double *lam, double Lam, const int32_t *pref, const double *g,
                      double *workload, double *dispatch, double *loss, cudaStream_t s);
 int tile_states();
+cudaError_t init_v2(const KArgs &k, int grid, cudaStream_t s);
 }  // namespace hqk_launch
 
 namespace {
@@ -103,12 +105,22 @@ TrieHost build_trie(int N, int J, const double *lam, const int32_t *pref) {
         const int v = order[p];
         for (auto &kv : t[v].child) size[v] += size[kv.second];
     }
+    std::vector<int> depth(t.size(), 0);
+    for (int p = 0; p < nn; p++) {
+        const int v = order[p];
+        for (auto &kv : t[v].child) depth[kv.second] = depth[v] + 1;
+    }
+    for (auto &kv : t[0].child) depth[kv.second] = 1;
+    for (int p = 0; p < nn; p++) {
+        const int v = order[p];
+        for (auto &kv : t[v].child) depth[kv.second] = depth[v] + 1;
+    }
     out.node.resize(nn);
     out.lam_thr.resize(nn);
     out.lam_end.resize(nn);
     for (int p = 0; p < nn; p++) {
         const int v = order[p];
-        out.node[p] = make_int2(t[v].unit, p + size[v]);
+        out.node[p] = make_int2(t[v].unit | (depth[v] << 8), p + size[v]);
         out.lam_thr[p] = t[v].thr;
         out.lam_end[p] = t[v].end;
     }
@@ -122,6 +134,37 @@ double binom(int n, int k) {
     return std::floor(r + 0.5);
 }
 
+// Internal unit order for the tile programs: units 0..7 vary inside a warp
+// tile, so they should be the units that least often precede other units in
+// the preference lists (fewest trie nodes with the unit on the path above
+// them): this minimises the per-state rate pairs.  perm[internal] = ABI unit.
+std::vector<int> choose_perm(int N, const TrieHost &tr) {
+    std::vector<int> perm(N);
+    for (int u = 0; u < N; u++) perm[u] = u;
+    const char *env = getenv("HQ_PERM");
+    if (N < 8 || (env && std::string(env) == "identity")) return perm;
+    std::vector<long> cnt(N, 0);
+    std::vector<int> stk;   // units on the current path (preorder + depth)
+    for (size_t v = 0; v < tr.node.size(); v++) {
+        const int u = tr.node[v].x & 0xff, d = (tr.node[v].x >> 8) & 0xff;
+        stk.resize(d - 1);
+        for (int a : stk) cnt[a]++;
+        stk.push_back(u);
+    }
+    std::vector<int> idx(N);
+    for (int u = 0; u < N; u++) idx[u] = u;
+    std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return cnt[a] < cnt[b]; });
+    std::vector<char> used(N, 0);
+    for (int i = 0; i < 8; i++) {
+        perm[i] = idx[i];
+        used[idx[i]] = 1;
+    }
+    int k = 8;
+    for (int u = 0; u < N; u++)
+        if (!used[u]) perm[k++] = u;
+    return perm;
+}
+
 }  // namespace
 
 struct hq_problem {
@@ -130,7 +173,9 @@ struct hq_problem {
     bool full_lists = true;
     std::vector<double> lam, mu;
     std::vector<int32_t> pref;
-    TrieHost trie;
+    TrieHost trie;                 // internal unit ids
+    std::vector<int> perm;         // internal unit -> ABI unit
+    std::vector<double> nu_int;    // service rates in internal order
     std::string err;
     int device = -1;
     int nsm = 0;
@@ -148,8 +193,30 @@ struct hq_problem {
     int *d_err = nullptr;
     double *h_small = nullptr;     // pinned mirror
     int grid = 0;
+    // v2 (N >= 8) device state
+    bool v2 = false, v2_ready = false;
+    uint32_t *d_order = nullptr, *d_off16 = nullptr, *d_size16 = nullptr;
+    uint4 *d_prog = nullptr;
+    double2 *d_omkap = nullptr;
+    double *d_lamarr = nullptr;
+    double *d_blk = nullptr, *h_blk = nullptr;
+    int sgrid = 0;
+    double prog_bytes = 0.0, precompute_ms = 0.0;
+    std::vector<cudaEvent_t> ev;   // per-half-sweep timing events (pairs), reused across solves
 
-    ~hq_problem() { release(); }
+    cudaEvent_t event(size_t i) {
+        while (ev.size() <= i) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            ev.push_back(e);
+        }
+        return ev[i];
+    }
+
+    ~hq_problem() {
+        release();
+        for (auto e : ev) cudaEventDestroy(e);
+    }
     void release() {
         cudaFree(d_node);
         cudaFree(d_lthr);
@@ -161,6 +228,19 @@ struct hq_problem {
         cudaFree(d_partial);
         cudaFree(d_small);
         cudaFree(d_err);
+        cudaFree(d_order);
+        cudaFree(d_off16);
+        cudaFree(d_size16);
+        cudaFree(d_prog);
+        cudaFree(d_omkap);
+        cudaFree(d_lamarr);
+        cudaFree(d_blk);
+        if (h_blk) cudaFreeHost(h_blk);
+        d_order = d_off16 = d_size16 = nullptr;
+        d_prog = nullptr;
+        d_omkap = nullptr;
+        d_lamarr = d_blk = h_blk = nullptr;
+        v2_ready = false;
         if (h_small) cudaFreeHost(h_small);
         d_node = nullptr;
         d_lthr = d_lend = d_lam = nullptr;
@@ -240,7 +320,18 @@ extern "C" hq_status hq_create(int N, int J, const double *lambda, const double 
     h->lam.assign(lambda, lambda + J);
     h->mu.assign(mu, mu + N);
     h->pref.assign(pref, pref + (size_t)J * N);
-    h->trie = build_trie(N, J, lambda, pref);
+    {
+        TrieHost abi = build_trie(N, J, lambda, pref);
+        h->perm = choose_perm(N, abi);
+        std::vector<int> inv(N);
+        for (int u = 0; u < N; u++) inv[h->perm[u]] = u;
+        std::vector<int32_t> pint((size_t)J * N);
+        for (size_t q = 0; q < pint.size(); q++) pint[q] = pref[q] < 0 ? -1 : inv[pref[q]];
+        h->trie = build_trie(N, J, lambda, pint.data());
+        h->nu_int.resize(N);
+        for (int u = 0; u < N; u++) h->nu_int[u] = mu[h->perm[u]];
+    }
+    h->v2 = N >= 8;
     *out = h.release();
     return HQ_OK;
 }
@@ -262,8 +353,10 @@ static hq_status ensure_device(hq_problem *h) {
     h->grid = (int)std::min<uint64_t>(ntiles, (uint64_t)h->nsm * 4);
     const size_t nn = h->trie.node.size();
     auto alloc = [&](void **p, size_t bytes) -> cudaError_t { return cudaMalloc(p, bytes ? bytes : 16); };
+    h->sgrid = hq2_launch::sweep_grid(h->nsm);
     if (alloc((void **)&h->d_pw, sizeof(double) * S) != cudaSuccess ||
-        alloc((void **)&h->d_ab, sizeof(double2) * (S >> 1 ? S >> 1 : 1)) != cudaSuccess) {
+        (!h->v2 && alloc((void **)&h->d_ab, sizeof(double2) * (S >> 1 ? S >> 1 : 1)) != cudaSuccess) ||
+        (h->v2 && alloc((void **)&h->d_omkap, sizeof(double2) * S) != cudaSuccess)) {
         cudaGetLastError();
         h->release();
         h->device = -1;
@@ -275,7 +368,9 @@ static hq_status ensure_device(hq_problem *h) {
     HQ_CUDA(alloc((void **)&h->d_lend, sizeof(double) * nn));
     HQ_CUDA(alloc((void **)&h->d_lam, sizeof(double) * h->J));
     HQ_CUDA(alloc((void **)&h->d_pref, sizeof(int32_t) * h->J * N));
-    HQ_CUDA(alloc((void **)&h->d_partial, sizeof(double) * 2 * h->grid * HQ_NL * HQ_NV));
+    HQ_CUDA(alloc((void **)&h->d_partial, sizeof(double) * 2 * std::max(h->grid, h->sgrid) * HQ_NL * HQ_NV));
+    HQ_CUDA(alloc((void **)&h->d_blk, sizeof(double) * V2S_TOTAL));
+    HQ_CUDA(cudaMallocHost((void **)&h->h_blk, sizeof(double) * V2S_TOTAL));
     HQ_CUDA(alloc((void **)&h->d_small, sizeof(double) * S_TOTAL));
     HQ_CUDA(alloc((void **)&h->d_err, sizeof(int)));
     HQ_CUDA(cudaMallocHost((void **)&h->h_small, sizeof(double) * S_TOTAL));
@@ -295,7 +390,7 @@ static KArgs base_args(hq_problem *h) {
     k.nstates_c = (uint64_t)1 << (h->N - 1);
     k.ntiles = (k.nstates_c + hqk_launch::tile_states() - 1) / hqk_launch::tile_states();
     k.Lam = h->Lam;
-    for (int i = 0; i < 32; i++) k.nu[i] = i < h->N ? h->mu[i] : 0.0;
+    for (int i = 0; i < 32; i++) k.nu[i] = i < h->N ? h->nu_int[i] : 0.0;
     k.trie.nnodes = (int)h->trie.node.size();
     k.trie.node = h->d_node;
     k.trie.lam_thr = h->d_lthr;
@@ -356,6 +451,236 @@ static hq_status true_residual(hq_problem *h, cudaStream_t s, double *res, int *
     return HQ_OK;
 }
 
+
+// ---------------------------------------------------------------------------
+// v2 path (N >= 8): precompute once per handle, then one kernel per half-sweep.
+// ---------------------------------------------------------------------------
+static hq_status v2_prepare(hq_problem *h, cudaStream_t s) {
+    if (h->v2_ready) return HQ_OK;
+    const int N = h->N;
+    const uint64_t S = 1ull << N, half = S >> 1;
+    const int Nt = N - 8;
+    const uint64_t ntiles = 1ull << Nt;
+    // tile visit order: by popcount of the tile index, ascending within a popcount class
+    std::vector<uint32_t> order;
+    order.reserve(ntiles);
+    for (int K = 0; K <= Nt; K++) {
+        if (K == 0) {
+            order.push_back(0);
+            continue;
+        }
+        uint64_t x = (1ull << K) - 1;
+        while (x < ntiles) {
+            order.push_back((uint32_t)x);
+            const uint64_t cc = x & (~x + 1), r = x + cc;
+            x = (((r ^ x) >> 2) / cc) | r;
+        }
+    }
+    auto alloc = [&](void **p, size_t bytes) -> cudaError_t { return cudaMalloc(p, bytes ? bytes : 16); };
+    if (alloc((void **)&h->d_order, 4 * ntiles) != cudaSuccess || alloc((void **)&h->d_off16, 4 * ntiles) != cudaSuccess ||
+        alloc((void **)&h->d_size16, 4 * ntiles) != cudaSuccess ||
+        (!h->full_lists && alloc((void **)&h->d_lamarr, 8 * S) != cudaSuccess)) {
+        cudaGetLastError();
+        h->err = "device memory for the tile tables could not be allocated";
+        return HQ_E_NOMEM;
+    }
+    HQ_CUDA(cudaMemcpyAsync(h->d_order, order.data(), 4 * ntiles, cudaMemcpyHostToDevice, s));
+    P2Args pa;
+    memset(&pa, 0, sizeof(pa));
+    pa.N = N;
+    pa.full_lists = h->full_lists ? 1 : 0;
+    pa.ntiles = ntiles;
+    pa.Lam = h->Lam;
+    for (int u = 0; u < 32; u++) pa.nu[u] = u < N ? h->nu_int[u] : 0.0;
+    pa.nnodes = (int)h->trie.node.size();
+    pa.node = h->d_node;
+    pa.lam_thr = h->d_lthr;
+    pa.lam_end = h->d_lend;
+    cudaEvent_t e0 = h->event(0), e1 = h->event(1);
+    HQ_CUDA(cudaEventRecord(e0, s));
+    const int g = h->nsm * 8;
+    if (!h->full_lists) HQ_CUDA(hq2_launch::lambda_states(pa, h->d_lamarr, g, s));
+    HQ_CUDA(hq2_launch::omkap(pa, h->d_lamarr, h->d_omkap, g, s));
+    HQ_CUDA(cudaMemsetAsync(h->d_err, 0, sizeof(int), s));
+    HQ_CUDA(hq2_launch::prog_count(pa, h->d_order, h->d_size16, h->d_err, g, s));
+    size_t tmpb = 0;
+    HQ_CUDA(hq2_launch::prog_scan(h->d_size16, h->d_off16, ntiles, nullptr, &tmpb, s));
+    void *tmp = nullptr;
+    HQ_CUDA(alloc(&tmp, tmpb));
+    HQ_CUDA(hq2_launch::prog_scan(h->d_size16, h->d_off16, ntiles, tmp, &tmpb, s));
+    uint32_t last[2] = {0, 0};
+    int herr = 0;
+    HQ_CUDA(cudaMemcpyAsync(&last[0], h->d_off16 + ntiles - 1, 4, cudaMemcpyDeviceToHost, s));
+    HQ_CUDA(cudaMemcpyAsync(&last[1], h->d_size16 + ntiles - 1, 4, cudaMemcpyDeviceToHost, s));
+    HQ_CUDA(cudaMemcpyAsync(&herr, h->d_err, sizeof(int), cudaMemcpyDeviceToHost, s));
+    HQ_CUDA(cudaStreamSynchronize(s));
+    cudaFree(tmp);
+    if (herr) {
+        h->err = "rate program overflow (too many distinct (unit, pattern) pairs in a tile)";
+        return HQ_E_NUMERIC;
+    }
+    const uint64_t total16 = (uint64_t)last[0] + last[1];
+    if (alloc((void **)&h->d_prog, 16 * total16) != cudaSuccess) {
+        cudaGetLastError();
+        h->err = "device memory for the rate programs could not be allocated";
+        return HQ_E_NOMEM;
+    }
+    HQ_CUDA(hq2_launch::prog_write(pa, h->d_order, h->d_off16, h->d_prog, g, s));
+    HQ_CUDA(cudaEventRecord(e1, s));
+    HQ_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    h->precompute_ms = ms;
+    h->prog_bytes = 16.0 * (double)total16;
+    cudaFree(h->d_size16);
+    h->d_size16 = nullptr;
+    (void)half;
+    h->v2_ready = true;
+    return HQ_OK;
+}
+
+struct SolveOut {
+    int sweeps = 0, halfsweeps = 0, launches = 0, nres = 0;
+    double updates = 0.0, sweep_ms = 0.0, resid_ms = 0.0, res = INFINITY;
+    bool converged = false;
+};
+
+static hq_status v2_residual(hq_problem *h, cudaStream_t s, S2Args sa, SolveOut &o) {
+    const int N = h->N;
+    const uint64_t half = 1ull << (N - 1);
+    cudaEvent_t ea = h->event(2 * (size_t)o.halfsweeps), eb = h->event(2 * (size_t)o.halfsweeps + 1);
+    HQ_CUDA(cudaEventRecord(ea, s));
+    for (int c = 0; c < 2; c++) {
+        sa.c = c;
+        sa.P = h->d_pw + (c ? half : 0);
+        sa.Q = h->d_pw + (c ? 0 : half);
+        sa.partial = h->d_partial + (size_t)c * h->sgrid * HQ_NL * HQ_NV;
+        HQ_CUDA(hq2_launch::sweep(sa, 2, h->sgrid, s));
+    }
+    HQ_CUDA(cudaEventRecord(eb, s));
+    HQ_CUDA(hq2_launch::scalars(N, sa.full_lists, h->Lam, 2, 0, 0, 2 * h->sgrid, h->d_partial, h->d_blk, s));
+    HQ_CUDA(cudaMemcpyAsync(h->h_blk, h->d_blk, sizeof(double) * V2S_TOTAL, cudaMemcpyDeviceToHost, s));
+    HQ_CUDA(cudaStreamSynchronize(s));
+    float x = 0.f;
+    cudaEventElapsedTime(&x, ea, eb);
+    o.resid_ms += x;
+    o.launches += 3;
+    o.nres++;
+    o.res = h->h_blk[V2S_MISC + 1];
+    return HQ_OK;
+}
+
+static hq_status solve_v2(hq_problem *h, double tol, int max_iter, double *pi, cudaStream_t s, SolveOut &o) {
+    hq_status st = v2_prepare(h, s);
+    if (st != HQ_OK) return st;
+    const int N = h->N;
+    const uint64_t half = 1ull << (N - 1);
+    double *hs = h->h_small;
+    // --- init (Algorithm 1 step 2)
+    for (int n = 0; n < 32; n++) hs[S_MUSTAR + n] = n <= N ? 1.0 / binom(N, n) : 0.0;
+    HQ_CUDA(cudaMemcpyAsync(h->d_small + S_MUSTAR, hs + S_MUSTAR, sizeof(double) * 32, cudaMemcpyHostToDevice, s));
+    HQ_CUDA(cudaMemsetAsync(h->d_blk, 0, sizeof(double) * V2S_TOTAL, s));
+    KArgs k = base_args(h);
+    for (int c = 0; c < 2; c++) {
+        class_arrays(h, k, c);
+        k.partial = h->d_partial + (size_t)c * h->grid * HQ_NL * HQ_NV;
+        k.omkap = h->d_omkap + (c ? half : 0);
+        k.lamarr = h->d_lamarr ? h->d_lamarr + (c ? half : 0) : nullptr;
+        HQ_CUDA(hqk_launch::init_v2(k, h->grid, s));
+    }
+    HQ_CUDA(hq2_launch::scalars(N, h->full_lists, h->Lam, 0, 0, 0, 2 * h->grid, h->d_partial, h->d_blk, s));
+    o.launches += 3;
+    if (getenv("HQ_DEBUG_INIT_ONLY")) {
+        HQ_CUDA(cudaStreamSynchronize(s));
+        o.res = 1.0;
+        return HQ_OK;
+    }
+
+    S2Args sa;
+    memset(&sa, 0, sizeof(sa));
+    sa.N = N;
+    sa.full_lists = h->full_lists ? 1 : 0;
+    sa.ntiles = 1ull << (N - 8);
+    sa.Lam = h->Lam;
+    for (int u = 0; u < 32; u++) sa.nu[u] = u < N ? h->nu_int[u] : 0.0;
+    sa.order = h->d_order;
+    sa.off16 = h->d_off16;
+    sa.prog = h->d_prog;
+    sa.coef = h->d_blk;
+    sa.partial = h->d_partial;
+
+    // convergence checks: the two half-sweeps before a check record |dp|
+    int next_check = N + 2 * 12;
+    double prev_proxy = -1.0;
+    int prev_check = 0;
+    for (int t = 1; N >= 2; t++) {
+        uint32_t active = 0;
+        for (int n = 1; n <= N - 1; n++)
+            if (((t - n) & 1) == 0 && n <= t && (t - n) / 2 < max_iter) active |= 1u << n;
+        if (!active) break;
+        const int c = t & 1;
+        sa.c = c;
+        sa.active = active;
+        sa.P = h->d_pw + (c ? half : 0);
+        sa.Q = h->d_pw + (c ? 0 : half);
+        sa.omkap = h->d_omkap + (c ? half : 0);
+        sa.partial = h->d_partial;
+        const bool checking = tol > 0.0 && t >= next_check - 1;
+        HQ_CUDA(cudaEventRecord(h->event(2 * (size_t)o.halfsweeps), s));
+        HQ_CUDA(hq2_launch::sweep(sa, checking ? 1 : 0, h->sgrid, s));
+        HQ_CUDA(cudaEventRecord(h->event(2 * (size_t)o.halfsweeps + 1), s));
+        HQ_CUDA(hq2_launch::scalars(N, sa.full_lists, h->Lam, 1, c, active, h->sgrid, h->d_partial, h->d_blk, s));
+        o.launches += 2;
+        o.halfsweeps++;
+        for (int n = 1; n <= N - 1; n++)
+            if ((active >> n) & 1u) o.updates += binom(N, n);
+        if ((active >> (N - 1)) & 1u) o.sweeps = (t - (N - 1)) / 2 + 1;
+        if (!checking || t < next_check) continue;
+        HQ_CUDA(cudaMemcpyAsync(h->h_blk, h->d_blk, sizeof(double) * V2S_TOTAL, cudaMemcpyDeviceToHost, s));
+        HQ_CUDA(cudaStreamSynchronize(s));
+        if (h->h_blk[V2S_MISC + 0] != 0.0) {
+            h->err = "non-positive or non-finite layer normaliser";
+            return HQ_E_NUMERIC;
+        }
+        const double proxy = h->h_blk[V2S_MISC + 2];
+        if (!std::isfinite(proxy)) {
+            h->err = "non-finite iterate";
+            return HQ_E_NUMERIC;
+        }
+        double rate = 0.0;   // per half-sweep decay factor
+        if (prev_proxy > 0.0 && t > prev_check) rate = std::pow(proxy / prev_proxy, 1.0 / (t - prev_check));
+        prev_proxy = proxy;
+        prev_check = t;
+        double level = proxy;
+        if (proxy <= 2.0 * tol) {
+            st = v2_residual(h, s, sa, o);
+            if (st != HQ_OK) return st;
+            if (o.res <= tol) {
+                o.converged = true;
+                break;
+            }
+            level = o.res;
+        }
+        int gap = 24;
+        if (rate > 0.0 && rate < 0.999) {
+            const double need = std::log(tol / level) / std::log(rate);
+            gap = std::max(2, (int)std::floor(0.9 * need));
+            gap = std::min(gap, 200);
+        }
+        next_check = t + gap;
+    }
+    if (!o.converged) {
+        st = v2_residual(h, s, sa, o);
+        if (st != HQ_OK) return st;
+        if (tol > 0.0 && o.res <= tol) o.converged = true;
+    }
+    HQ_CUDA(hq2_launch::assemble(N, h->d_pw, h->d_blk + V2S_PN, h->perm.data(), pi, h->nsm * 8, s));
+    o.launches++;
+    // layer masses for the stats
+    for (int n = 0; n <= N; n++) hs[S_PN + n] = h->h_blk[V2S_PN + n + 1];
+    return HQ_OK;
+}
+
 extern "C" hq_status hq_solve(hq_handle h, double tol, int max_iter, double *pi, void *cuda_stream, int *iters_out,
                               double *residual_out) {
     if (!h) return HQ_E_INVAL;
@@ -373,6 +698,57 @@ extern "C" hq_status hq_solve(hq_handle h, double tol, int max_iter, double *pi,
     const int N = h->N;
     const size_t S = (size_t)1 << N;
     double *hs = h->h_small;
+    if (h->v2) {
+        cudaEvent_t a0, a1;
+        HQ_CUDA(cudaEventCreate(&a0));
+        HQ_CUDA(cudaEventCreate(&a1));
+        HQ_CUDA(cudaEventRecord(a0, s));
+        SolveOut o;
+        st = solve_v2(h, tol, max_iter, pi, s, o);
+        if (st != HQ_OK) {
+            cudaEventDestroy(a0);
+            cudaEventDestroy(a1);
+            return st;
+        }
+        HQ_CUDA(cudaEventRecord(a1, s));
+        HQ_CUDA(cudaEventSynchronize(a1));
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, a0, a1);
+        cudaEventDestroy(a0);
+        cudaEventDestroy(a1);
+        double sweep_ms = 0.0;
+        for (int i = 0; i < o.halfsweeps; i++) {
+            float x = 0.f;
+            cudaEventElapsedTime(&x, h->ev[2 * i], h->ev[2 * i + 1]);
+            sweep_ms += x;
+        }
+        double sp = 0.0;
+        for (int n = 0; n <= N; n++) sp += hs[S_PN + n];
+        memset(h->stats, 0, sizeof(h->stats));
+        h->stats[0] = o.sweeps;
+        h->stats[1] = o.halfsweeps;
+        h->stats[2] = o.updates;
+        h->stats[3] = o.launches;
+        h->stats[4] = o.nres;
+        h->stats[5] = (double)h->trie.node.size();
+        h->stats[6] = sp - 1.0;
+        h->stats[7] = ms;
+        h->stats[8] = sweep_ms;
+        h->stats[9] = o.halfsweeps;
+        h->stats[10] = o.resid_ms;
+        h->stats[11] = h->precompute_ms;
+        h->stats[12] = h->prog_bytes;
+        h->stats[13] = 2;   // path id
+        if (iters_out) *iters_out = o.sweeps;
+        if (residual_out) *residual_out = o.res;
+        if (!std::isfinite(o.res)) {
+            h->err = "non-finite residual";
+            return HQ_E_NUMERIC;
+        }
+        h->solved = true;
+        if (tol <= 0.0) return HQ_OK;
+        return o.converged ? HQ_OK : HQ_NOT_CONVERGED;
+    }
     cudaEvent_t e0, e1;
     HQ_CUDA(cudaEventCreate(&e0));
     HQ_CUDA(cudaEventCreate(&e1));
@@ -411,10 +787,12 @@ extern "C" hq_status hq_solve(hq_handle h, double tol, int max_iter, double *pi,
         class_arrays(h, k, c);
         k.active = active;
         k.partial = h->d_partial;
+        HQ_CUDA(cudaEventRecord(h->event(2 * (size_t)halfsweeps), s));
         HQ_CUDA(hqk_launch::gather(k, h->grid, s));
         HQ_CUDA(hqk_launch::layer_reduce(N, active, h->grid, 1, h->d_partial, 6, 0, h->d_small + S_LAM,
                                          h->d_small + S_MU, h->d_small + S_MUSTAR, nullptr, h->d_err, s));
         HQ_CUDA(hqk_launch::finalize(k, h->grid, s));
+        HQ_CUDA(cudaEventRecord(h->event(2 * (size_t)halfsweeps + 1), s));
         HQ_CUDA(hqk_launch::layer_reduce(N, active, h->grid, 1, h->d_partial, 3, 1, nullptr, nullptr, nullptr,
                                          h->d_small + S_STATS, h->d_err, s));
         launches += 4;
@@ -471,6 +849,12 @@ extern "C" hq_status hq_solve(hq_handle h, double tol, int max_iter, double *pi,
     HQ_CUDA(cudaEventSynchronize(e1));
     float ms = 0.f;
     cudaEventElapsedTime(&ms, e0, e1);
+    double sweep_ms = 0.0;
+    for (int i = 0; i < halfsweeps; i++) {
+        float x = 0.f;
+        cudaEventElapsedTime(&x, h->ev[2 * i], h->ev[2 * i + 1]);
+        sweep_ms += x;
+    }
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     int herr = 0;
@@ -490,6 +874,9 @@ extern "C" hq_status hq_solve(hq_handle h, double tol, int max_iter, double *pi,
     h->stats[5] = (double)h->trie.node.size();
     h->stats[6] = sp - 1.0;
     h->stats[7] = ms;
+    h->stats[8] = sweep_ms;
+    h->stats[9] = 2.0 * halfsweeps;   // gather + finalize launches
+    h->stats[13] = 1;   // path id
     if (iters_out) *iters_out = sweeps;
     if (residual_out) *residual_out = res;
     if (!std::isfinite(res)) {
@@ -518,7 +905,7 @@ extern "C" hq_status hq_measures(hq_handle h, const double *pi, double *workload
     cudaStream_t s = (cudaStream_t)cuda_stream;
     const int N = h->N;
     const size_t S = (size_t)1 << N;
-    double *g = reinterpret_cast<double *>(h->d_ab);   // 2^(N-1) double2 == 2^N doubles
+    double *g = h->d_pw;   // p is re-initialised by every hq_solve, so it can hold the superset sums
     HQ_CUDA(cudaMemcpyAsync(g, pi, sizeof(double) * S, cudaMemcpyDeviceToDevice, s));
     HQ_CUDA(hqk_launch::zeta(N, g, h->nsm * 8, s));
     HQ_CUDA(hqk_launch::measures(N, h->J, h->d_lam, h->Lam, h->d_pref, g, workload, dispatch,
@@ -539,6 +926,30 @@ extern "C" hq_status hq_stats(hq_handle h, double *out) {
     if (!h || !out) return HQ_E_INVAL;
     memcpy(out, h->stats, sizeof(h->stats));
     return HQ_OK;
+}
+
+// Debug/introspection copy of internal device arrays (tests only).
+//   which: 0 v2 scalar block, 1 p (parity-compressed), 2 (omega, kappa),
+//          3 rate programs, 4 program offsets, 5 tile order, 6 internal->ABI unit map (host)
+extern "C" hq_status hq_debug_copy(hq_handle h, int which, void *host, size_t bytes) {
+    if (!h || !host) return HQ_E_INVAL;
+    const void *src = nullptr;
+    if (which == 6) {
+        memcpy(host, h->perm.data(), std::min(bytes, sizeof(int) * h->perm.size()));
+        return HQ_OK;
+    }
+    switch (which) {
+        case 0: src = h->d_blk; break;
+        case 1: src = h->d_pw; break;
+        case 2: src = h->d_omkap; break;
+        case 3: src = h->d_prog; break;
+        case 4: src = h->d_off16; break;
+        case 5: src = h->d_order; break;
+        default: return HQ_E_INVAL;
+    }
+    if (!src) return HQ_E_ORDER;
+    cudaError_t e = cudaMemcpy(host, src, bytes, cudaMemcpyDeviceToHost);
+    return e == cudaSuccess ? HQ_OK : HQ_E_CUDA;
 }
 
 extern "C" const char *hq_version(void) { return "hq-b200 0.1 (sm_100a, fp64, red-black staggered Algorithm 1)"; }

@@ -61,4 +61,6 @@ struct KArgs {
     const double *mustar;    // [HQ_NL] mu*(n) of this half-sweep
     const double *pn;        // [HQ_NL] layer masses p(n) (residual / assembly)
     double *partial;         // [grid][HQ_NL][HQ_NV]
+    const double2 *omkap;    // v2 init: scatter weights of class c
+    const double *lamarr;    // v2 init (truncated lists): lambda_m of class c, or NULL
 };

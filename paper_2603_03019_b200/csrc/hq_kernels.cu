@@ -58,8 +58,9 @@ __device__ __forceinline__ Gathered gather_state(const KArgs &k, uint32_t j, uin
     const int nn = k.trie.nnodes;
     while (v < nn) {
         int2 nd = __ldg(&node[v]);
-        if ((m >> nd.x) & 1u) {
-            W[nd.x] += __ldg(&lthr[v]);
+        const int nu_ = nd.x & 0xff;
+        if ((m >> nu_) & 1u) {
+            W[nu_] += __ldg(&lthr[v]);
             if (!k.full_lists) blocked += __ldg(&lend[v]);
             v++;
         } else {
@@ -224,7 +225,7 @@ __global__ void __launch_bounds__(HQ_BLOCK) k_init(KArgs k) {
             int v = 0;
             while (v < k.trie.nnodes) {
                 int2 nd = k.trie.node[v];
-                if ((m >> nd.x) & 1u) {
+                if ((m >> (nd.x & 0xff)) & 1u) {
                     blocked += k.trie.lam_end[v];
                     v++;
                 } else {
@@ -237,6 +238,32 @@ __global__ void __launch_bounds__(HQ_BLOCK) k_init(KArgs k) {
             if ((m >> u) & 1u) mu += k.nu[u];
         vals[0] = lam * p;
         vals[1] = mu * p;
+        return true;
+    });
+}
+
+// v2 init: p_n(m) = 1/C(N,n) and the layer sums {p, p mu_m, p omega, p kappa,
+// p lambda_m} that seed the a-priori normalisation of the first half-sweep.
+template <int R>
+__global__ void __launch_bounds__(HQ_BLOCK) k_init_v2(KArgs k) {
+    tile_loop<R, 5>(k, k.partial, [&](uint32_t j, double *vals) -> bool {
+        int n;
+        uint32_t m;
+        decode(k, j, n, m);
+        const double p = k.mustar[n];
+        k.P[j] = p;
+        double lam;
+        if (k.full_lists) lam = (n == k.N) ? 0.0 : k.Lam;
+        else lam = k.lamarr[j];
+        double mu = 0.0;
+        for (int u = 0; u < k.N; u++)
+            if ((m >> u) & 1u) mu += k.nu[u];
+        const double2 ok = k.omkap[j];
+        vals[0] = p;
+        vals[1] = p * mu;
+        vals[2] = p * ok.x;
+        vals[3] = p * ok.y;
+        vals[4] = p * lam;
         return true;
     });
 }
@@ -399,6 +426,10 @@ cudaError_t finalize(const KArgs &k, int grid, cudaStream_t s) {
 }
 cudaError_t init(const KArgs &k, int grid, cudaStream_t s) {
     hqk::k_init<R><<<grid, HQ_BLOCK, red_smem(2), s>>>(k);
+    return cudaGetLastError();
+}
+cudaError_t init_v2(const KArgs &k, int grid, cudaStream_t s) {
+    hqk::k_init_v2<R><<<grid, HQ_BLOCK, red_smem(5), s>>>(k);
     return cudaGetLastError();
 }
 cudaError_t residual(const KArgs &k, int grid, cudaStream_t s) {

@@ -1,0 +1,633 @@
+// hq_v2.cu -- the production sweep path (N >= 8) of the B200 solver.
+//
+// Design:
+//  * Work unit = a warp tile of 128 parity-compressed states: compressed bits
+//    0..4 are the lanes, bits 5..6 four register states per thread.  In the
+//    internal unit order, units 0..7 vary inside a tile (unit 0 is the implied
+//    parity bit, units 1..5 the lane bits, units 6..7 the register bits) and
+//    units 8..N-1 are fixed by the tile index t (unit u <-> bit u-8 of t).
+//  * Upward rates (Eq. tran_rates) never exist as a table.
+//    Per tile a "rate program" is precomputed once per instance: for every
+//    unit u the tile-uniform part W0_u = sum of Lambda_v over trie nodes of
+//    unit u whose predecessor path is satisfied by the tile's fixed units and
+//    uses no varying unit, plus a short list of (S, c) pairs, S = the varying
+//    units the path needs.  W_u(m) = W0_u + sum_{S subset of m} c.  This is
+//    Algorithm 3 evaluated symbolically for 128 states.
+//  * Normalisation a priori: the closed-form inner fixed point of Algorithm 1
+//    mu*(n) = (1 - sum_m b_m)/sum_m a_m (R1) is obtained BEFORE the
+//    layer is touched from per-state scatter weights
+//        omega(l) = sum_{i not in l} lambda_{l, l+i} / den(l+i),
+//        kappa(l) = sum_{i in l}     nu_i              / den(l-i),
+//    since sum_{m in C_n} a_m = sum_{l in C_{n-1}} p(l) omega(l) / lambda(n-1)
+//    and sum_{m in C_n} b_m = lambda(n)/mu(n+1) sum_{l in C_{n+1}} p(l) kappa(l)
+//    (exact reindexing of the sums in Eq. updateHeter).  So one pass per
+//    half-sweep writes p_n(m) = (alpha_n A(m) + beta_n D(m)) / den(m) directly,
+//    alpha_n = mu*(n)/lambda(n-1), beta_n = lambda(n)/mu(n+1).
+//  * Tiles are visited in order of popcount(t) so that per-layer sums are kept
+//    in 3 register bins per thread; the order also keeps the neighbour class
+//    L2-resident up to N ~ 26.
+#include <cuda_runtime.h>
+#include <cub/cub.cuh>
+#include <cstdint>
+#include "hq_internal.h"
+#include "hq_v2.h"
+
+namespace hq2 {
+
+__device__ __forceinline__ double warp_sum(double s) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    return s;
+}
+
+// ---------------------------------------------------------------------------
+// Precompute 1: lambda_m for truncated lists (temp array, compressed layout).
+// ---------------------------------------------------------------------------
+__global__ void k_lambda_states(P2Args a, double *__restrict__ lamarr) {
+    const uint64_t half = 1ull << (a.N - 1);
+    for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < 2 * half;
+         x += (uint64_t)gridDim.x * blockDim.x) {
+        const int c = (int)(x >= half);
+        const uint32_t j = (uint32_t)(x - (c ? half : 0));
+        const int b0 = c ^ (__popc(j) & 1);
+        const uint32_t m = (j << 1) | (uint32_t)b0;
+        double blocked = 0.0;
+        int v = 0;
+        while (v < a.nnodes) {
+            const int2 nd = __ldg(&a.node[v]);
+            if ((m >> (nd.x & 0xff)) & 1u) {
+                blocked += __ldg(&a.lam_end[v]);
+                v++;
+            } else {
+                v = nd.y;
+            }
+        }
+        lamarr[x] = a.Lam - blocked;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Precompute 2: scatter weights omega(l), kappa(l) for every state.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double lam_of(const P2Args &a, const double *lamarr, uint32_t m) {
+    if (a.full_lists) return (m == (1u << a.N) - 1u) ? 0.0 : a.Lam;
+    const uint64_t half = 1ull << (a.N - 1);
+    const int c = __popc(m) & 1;
+    return lamarr[(c ? half : 0) + (m >> 1)];
+}
+
+__global__ void k_omkap(P2Args a, const double *__restrict__ lamarr, double2 *__restrict__ omkap) {
+    const uint64_t half = 1ull << (a.N - 1);
+    for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < 2 * half;
+         x += (uint64_t)gridDim.x * blockDim.x) {
+        const int c = (int)(x >= half);
+        const uint32_t j = (uint32_t)(x - (c ? half : 0));
+        const int b0 = c ^ (__popc(j) & 1);
+        const uint32_t l = (j << 1) | (uint32_t)b0;
+        double up[HQ_MAXN + 1];
+        for (int u = 0; u <= HQ_MAXN; u++) up[u] = 0.0;
+        // out-rates of l: every atom goes to its first free unit (frontier nodes)
+        int v = 0;
+        while (v < a.nnodes) {
+            const int2 nd = __ldg(&a.node[v]);
+            const int u = nd.x & 0xff;
+            if ((l >> u) & 1u) {
+                v++;
+            } else {
+                up[u] += __ldg(&a.lam_thr[v]);
+                v = nd.y;
+            }
+        }
+        double mul = 0.0;
+        for (int u = 0; u < a.N; u++)
+            if ((l >> u) & 1u) mul += a.nu[u];
+        double om = 0.0, ka = 0.0;
+        for (int u = 0; u < a.N; u++) {
+            const uint32_t nb = l ^ (1u << u);
+            if ((l >> u) & 1u) {
+                const double den = lam_of(a, lamarr, nb) + (mul - a.nu[u]);
+                ka += a.nu[u] / den;
+            } else if (up[u] != 0.0) {
+                const double den = lam_of(a, lamarr, nb) + (mul + a.nu[u]);
+                om += up[u] / den;
+            }
+        }
+        omkap[x] = make_double2(om, ka);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Precompute 3: per-tile rate programs.
+// ---------------------------------------------------------------------------
+struct PairAcc {
+    int n;
+    uint16_t key[PROG_MAXPAIRS];   // unit | S << 6
+    double val[PROG_MAXPAIRS];
+};
+
+__device__ __forceinline__ bool pair_add(PairAcc &P, double *W0, int u, uint32_t S, double val) {
+    if (S == 0) {
+        W0[u] += val;
+        return true;
+    }
+    const uint16_t key = (uint16_t)(u | (S << 6));
+    for (int i = 0; i < P.n; i++)
+        if (P.key[i] == key) {
+            P.val[i] += val;
+            return true;
+        }
+    if (P.n >= PROG_MAXPAIRS) return false;
+    P.key[P.n] = key;
+    P.val[P.n] = val;
+    P.n++;
+    return true;
+}
+
+// Walk the trie for tile t (fixed units 8.. given by F = t << 8).
+__device__ bool tile_walk(const P2Args &a, uint32_t F, double *W0, PairAcc &P) {
+    uint32_t Sst[HQ_MAXN + 2];
+    Sst[0] = 0;
+    for (int u = 0; u <= HQ_MAXN; u++) W0[u] = 0.0;
+    P.n = 0;
+    int v = 0;
+    while (v < a.nnodes) {
+        const int2 nd = __ldg(&a.node[v]);
+        const int u = nd.x & 0xff;
+        const int d = (nd.x >> 8) & 0xff;
+        if (u >= PROG_NVARY && !((F >> u) & 1u)) {   // fixed and free: dead subtree
+            v = nd.y;
+            continue;
+        }
+        const uint32_t Spre = Sst[d - 1];
+        if (!pair_add(P, W0, u, Spre, __ldg(&a.lam_thr[v]))) return false;
+        const uint32_t Sme = Spre | (u < PROG_NVARY ? (1u << u) : 0u);
+        if (!a.full_lists) {
+            const double e = __ldg(&a.lam_end[v]);
+            if (e != 0.0 && !pair_add(P, W0, a.N, Sme, e)) return false;
+        }
+        Sst[d] = Sme;
+        v++;
+    }
+    return true;
+}
+
+__global__ void k_prog_count(P2Args a, const uint32_t *__restrict__ order, uint32_t *__restrict__ size16,
+                             int *__restrict__ err) {
+    PairAcc P;
+    double W0[HQ_MAXN + 1];
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.ntiles;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t t = order[i];
+        if (!tile_walk(a, t << 8, W0, P)) {
+            atomicExch(err, 2);
+            size16[i] = PROG_HDR16;
+            continue;
+        }
+        int cnt[HQ_MAXN + 1];
+        for (int u = 0; u <= HQ_MAXN; u++) cnt[u] = 0;
+        for (int k = 0; k < P.n; k++) cnt[P.key[k] & 63]++;
+        for (int u = 0; u <= HQ_MAXN; u++)
+            if (cnt[u] > 255) atomicExch(err, 3);
+        size16[i] = PROG_HDR16 + (uint32_t)P.n;
+    }
+}
+
+__global__ void k_prog_write(P2Args a, const uint32_t *__restrict__ order, const uint32_t *__restrict__ off16,
+                             uint4 *__restrict__ prog) {
+    PairAcc P;
+    double W0[HQ_MAXN + 1];
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.ntiles;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t t = order[i];
+        uint4 *out = prog + off16[i];
+        if (!tile_walk(a, t << 8, W0, P)) continue;
+        // stable sort of the pairs by unit (insertion sort, DFS order kept within a unit)
+        for (int x = 1; x < P.n; x++) {
+            const uint16_t k = P.key[x];
+            const double vv = P.val[x];
+            int y = x - 1;
+            while (y >= 0 && (P.key[y] & 63) > (k & 63)) {
+                P.key[y + 1] = P.key[y];
+                P.val[y + 1] = P.val[y];
+                y--;
+            }
+            P.key[y + 1] = k;
+            P.val[y + 1] = vv;
+        }
+        uint32_t cw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int k = 0; k < P.n; k++) {
+            const int u = P.key[k] & 63;
+            cw[u >> 2] += 1u << ((u & 3) * 8);
+        }
+        out[0] = make_uint4(cw[0], cw[1], cw[2], cw[3]);
+        out[1] = make_uint4(cw[4], cw[5], cw[6], cw[7]);
+        double *w0o = reinterpret_cast<double *>(out + 2);
+        for (int u = 0; u < 32; u++) w0o[u] = u <= HQ_MAXN ? W0[u] : 0.0;
+        for (int k = 0; k < P.n; k++) {
+            const uint32_t S = P.key[k] >> 6;
+            const int u = P.key[k] & 63;
+            const uint32_t s0 = S & 1u, slane = (S >> 1) & 31u, sreg = (S >> 6) & 3u;
+            uint32_t rm[2] = {0, 0};
+            for (int beta = 0; beta < 2; beta++)
+                for (int r = 0; r < 4; r++) {
+                    const uint32_t b0 = (uint32_t)beta ^ (uint32_t)(__popc(r) & 1);
+                    if ((sreg & ~(uint32_t)r) == 0 && (!s0 || b0)) rm[beta] |= 1u << r;
+                }
+            const uint32_t w = slane | (rm[0] << 8) | (rm[1] << 12) | ((uint32_t)u << 16);
+            const double c = P.val[k];
+            out[PROG_HDR16 + k] = make_uint4((uint32_t)__double_as_longlong(c),
+                                             (uint32_t)(__double_as_longlong(c) >> 32), w, 0u);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// The sweep / residual kernel.
+//   MODE 0: sweep (write p of the active layers of class c)
+//   MODE 1: sweep + per-layer sum |p_new - p_old| (convergence proxy)
+//   MODE 2: residual of Eq. balance_eq_heter for the states of class c
+// ---------------------------------------------------------------------------
+constexpr int WARPS = 8;
+
+template <int MODE>
+__device__ __forceinline__ void flush_bins(double (&bins)[3][NV2], int K, int c, int pcl, int lane,
+                                           double (*wacc)[NV2]) {
+    if (K < 0) return;
+    // bin k of this lane holds layer L_k = K + pcl + k + ((c ^ K ^ pcl ^ k) & 1)
+    const int Lmin = K + ((c ^ K) & 1);   // smallest layer of parity c that can occur
+    int Lk[3];
+#pragma unroll
+    for (int k = 0; k < 3; k++) Lk[k] = K + pcl + k + ((c ^ K ^ pcl ^ k) & 1);
+    for (int d = 0; d < 5; d++) {
+        const int L = Lmin + 2 * d;
+        if (L >= HQ_NL) break;
+        const bool any = (Lk[0] == L) || (Lk[1] == L) || (Lk[2] == L);
+        if (!__any_sync(0xffffffffu, any)) continue;
+#pragma unroll
+        for (int v = 0; v < NV2; v++) {
+            double s = 0.0;
+#pragma unroll
+            for (int k = 0; k < 3; k++) s += (Lk[k] == L) ? bins[k][v] : 0.0;
+            s = warp_sum(s);
+            if (lane == 0) wacc[L][v] += s;
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < 3; k++)
+#pragma unroll
+        for (int v = 0; v < NV2; v++) bins[k][v] = 0.0;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(WARPS * 32, 2) k_sweep2(S2Args a) {
+    __shared__ double s_x[32];       // alpha(n) (sweep) or p(n-1) (residual, shifted)
+    __shared__ double s_y[32];       // beta(n)  (sweep) or p(n+1)
+    __shared__ double s_z[32];       // unused (sweep) or p(n)
+    __shared__ double wacc[WARPS][HQ_NL][NV2];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int i = tid; i < WARPS * HQ_NL * NV2; i += blockDim.x) (&wacc[0][0][0])[i] = 0.0;
+    if (tid < 32) {
+        if (MODE == 2) {
+            const double *pn1 = a.coef + V2S_PN;   // pn1[n + 1] = p(n)
+            s_x[tid] = pn1[tid];                   // p(n - 1)
+            s_y[tid] = tid + 2 < 34 ? pn1[tid + 2] : 0.0;   // p(n + 1)
+            s_z[tid] = pn1[tid + 1];               // p(n)
+        } else {
+            s_x[tid] = a.coef[V2S_ALPHA + tid];
+            s_y[tid] = a.coef[V2S_BETA + tid];
+            s_z[tid] = 0.0;
+        }
+    }
+    __syncthreads();
+
+    const int pcl = __popc(lane);
+    const uint64_t nwarps = (uint64_t)gridDim.x * WARPS;
+    const uint64_t gw = (uint64_t)blockIdx.x * WARPS + warp;
+    const uint64_t chunk = (a.ntiles + nwarps - 1) / nwarps;
+    const uint64_t i0 = gw * chunk;
+    const uint64_t i1 = min(i0 + chunk, a.ntiles);
+    const uint32_t fullm = (a.N >= 32) ? 0xffffffffu : ((1u << a.N) - 1u);
+
+    // per-lane constants: service rate of the lane units (1..5) that are busy
+    double mu_lane = 0.0;
+#pragma unroll
+    for (int b = 0; b < 5; b++)
+        if ((lane >> b) & 1) mu_lane += a.nu[1 + b];
+
+    double bins[3][NV2];
+#pragma unroll
+    for (int k = 0; k < 3; k++)
+#pragma unroll
+        for (int v = 0; v < NV2; v++) bins[k][v] = 0.0;
+    int curK = -1;
+
+    for (uint64_t i = i0; i < i1; i++) {
+        const uint32_t t = __ldg(a.order + i);
+        const int K = __popc(t);
+        if (K != curK) {
+            flush_bins<MODE>(bins, curK, a.c, pcl, lane, wacc[warp]);
+            curK = K;
+        }
+        const uint32_t jb = t << PROG_TB;
+        const int beta = (a.c ^ K ^ pcl) & 1;
+        const double *__restrict__ Q = a.Q;
+        double qo[4];
+#pragma unroll
+        for (int r = 0; r < 4; r++) qo[r] = __ldg(Q + jb + r * 32 + lane);
+        double pold[4];
+        if (MODE != 0) {
+#pragma unroll
+            for (int r = 0; r < 4; r++) pold[r] = a.P[jb + r * 32 + lane];
+        }
+        const uint4 *__restrict__ pg = a.prog + __ldg(a.off16 + i);
+        const uint4 h0 = __ldg(pg), h1 = __ldg(pg + 1);
+        const uint32_t cw[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+        const double *__restrict__ w0 = reinterpret_cast<const double *>(pg + 2);
+        int pp = PROG_HDR16;
+        double A[4] = {0.0, 0.0, 0.0, 0.0}, D[4] = {0.0, 0.0, 0.0, 0.0};
+        double mu_fix = 0.0;
+
+#pragma unroll
+        for (int u = 0; u < HQ_MAXN; u++) {
+            if (u >= a.N) break;
+            const int cnt = (int)((cw[u >> 2] >> ((u & 3) * 8)) & 0xffu);
+            const bool fixed = u >= PROG_NVARY;
+            const bool fbusy = fixed && ((t >> (u - PROG_NVARY)) & 1u);
+            double q[4];
+            if (u == 0) {
+#pragma unroll
+                for (int r = 0; r < 4; r++) q[r] = qo[r];
+            } else if (u <= 5) {
+#pragma unroll
+                for (int r = 0; r < 4; r++) q[r] = __shfl_xor_sync(0xffffffffu, qo[r], 1 << (u - 1));
+            } else if (u <= 7) {
+#pragma unroll
+                for (int r = 0; r < 4; r++) q[r] = qo[r ^ (1 << (u - 6))];
+            } else {
+                const double *__restrict__ qn = Q + (jb ^ (1u << (u - 1))) + lane;
+#pragma unroll
+                for (int r = 0; r < 4; r++) q[r] = __ldg(qn + r * 32);
+            }
+            const double nu = a.nu[u];
+            if (fixed && !fbusy) {
+#pragma unroll
+                for (int r = 0; r < 4; r++) D[r] = fma(nu, q[r], D[r]);
+                continue;
+            }
+            double W[4];
+            const double wu = __ldg(w0 + u);
+#pragma unroll
+            for (int r = 0; r < 4; r++) W[r] = wu;
+            for (int k = 0; k < cnt; k++) {
+                const uint4 rec = __ldg(pg + pp + k);
+                const double cc = __hiloint2double((int)rec.y, (int)rec.x);
+                const uint32_t w = rec.z;
+                const bool tl = ((w & 31u) & ~(uint32_t)lane) == 0u;
+                const uint32_t m4 = tl ? ((w >> (8 + 4 * beta)) & 15u) : 0u;
+#pragma unroll
+                for (int r = 0; r < 4; r++)
+                    if ((m4 >> r) & 1u) W[r] += cc;
+            }
+            pp += cnt;
+            if (fixed) {
+                mu_fix += nu;
+#pragma unroll
+                for (int r = 0; r < 4; r++) A[r] = fma(W[r], q[r], A[r]);
+            } else {
+#pragma unroll
+                for (int r = 0; r < 4; r++) {
+                    const int b0r = beta ^ (__popc(r) & 1);
+                    const bool busy = (u == 0) ? (b0r != 0) : (u <= 5) ? (((lane >> (u - 1)) & 1) != 0)
+                                                                       : (((r >> (u - 6)) & 1) != 0);
+                    if (busy) A[r] = fma(W[r], q[r], A[r]);
+                    else D[r] = fma(nu, q[r], D[r]);
+                }
+            }
+        }
+        // blocked pseudo-unit (truncated lists): lambda_m = Lambda - blocked
+        double lam[4];
+        if (a.full_lists) {
+#pragma unroll
+            for (int r = 0; r < 4; r++) lam[r] = a.Lam;
+        } else {
+            const int u = a.N;
+            uint32_t word = 0;
+#pragma unroll
+            for (int q = 0; q < 8; q++)
+                if (q == (u >> 2)) word = cw[q];
+            const int cnt = (int)((word >> ((u & 3) * 8)) & 0xffu);
+            const double wu = __ldg(w0 + u);
+            double Bk[4] = {wu, wu, wu, wu};
+            for (int k = 0; k < cnt; k++) {
+                const uint4 rec = __ldg(pg + pp + k);
+                const double cc = __hiloint2double((int)rec.y, (int)rec.x);
+                const uint32_t w = rec.z;
+                const bool tl = ((w & 31u) & ~(uint32_t)lane) == 0u;
+                const uint32_t m4 = tl ? ((w >> (8 + 4 * beta)) & 15u) : 0u;
+#pragma unroll
+                for (int r = 0; r < 4; r++)
+                    if ((m4 >> r) & 1u) Bk[r] += cc;
+            }
+#pragma unroll
+            for (int r = 0; r < 4; r++) lam[r] = a.Lam - Bk[r];
+        }
+        const double2 *__restrict__ okp = a.omkap;
+#pragma unroll
+        for (int r = 0; r < 4; r++) {
+            const int pr = __popc(r);
+            const int b0r = beta ^ (pr & 1);
+            const int n = K + pcl + pr + b0r;
+            const uint32_t j = jb + r * 32 + lane;
+            double mu = mu_fix + mu_lane + (b0r ? a.nu[0] : 0.0) + ((r & 1) ? a.nu[6] : 0.0) + ((r & 2) ? a.nu[7] : 0.0);
+            double lm = lam[r];
+            if (a.full_lists && ((((j << 1) | (uint32_t)b0r)) == fullm)) lm = 0.0;
+            const double den = lm + mu;
+            const double rden = __drcp_rn(den);
+            if (MODE == 2) {
+                const double out = s_z[n] * pold[r] * den;
+                const double in = s_x[n] * A[r] + s_y[n] * D[r];
+                bins[pr][V2_RNUM] += fabs(out - in);
+                bins[pr][V2_RDEN] += out;
+            } else {
+                if (!((a.active >> n) & 1u)) continue;
+                const double p = (s_x[n] * A[r] + s_y[n] * D[r]) * rden;
+                a.P[j] = p;
+                const double2 ok = __ldg(okp + j);
+                bins[pr][V2_P] += p;
+                bins[pr][V2_OM] += p * ok.x;
+                bins[pr][V2_KA] += p * ok.y;
+                bins[pr][V2_LAM] += p * lm;
+                if (MODE == 1) bins[pr][V2_DL1] += fabs(p - pold[r]);
+            }
+        }
+    }
+    flush_bins<MODE>(bins, curK, a.c, pcl, lane, wacc[warp]);
+    __syncthreads();
+    double *out = a.partial + (size_t)blockIdx.x * HQ_NL * HQ_NV;
+    for (int i = tid; i < HQ_NL * NV2; i += blockDim.x) {
+        const int L = i / NV2, v = i % NV2;
+        double s = 0.0;
+#pragma unroll
+        for (int w = 0; w < WARPS; w++) s += wacc[w][L][v];
+        out[L * HQ_NV + v] = s;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Layer scalars (one block, warp n reduces layer n over the CTA partials).
+//   mode 0 (init), 1 (after a sweep half-sweep), 2 (after a residual pass).
+// After modes 0/1 the coefficients alpha(n), beta(n) of the next half-sweep
+// (class 1 - c) are prepared:
+//   beta(n)  = lambda(n) / mu(n+1)
+//   alpha(n) = mu*(n) / lambda(n-1) = (1 - beta(n) S_kappa(n+1)) / S_omega(n-1)
+// and p(n) (Eq. bnd_stationary) is refreshed.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) k_scalars2(int N, int full_lists, double Lam, int mode, int c, uint32_t active,
+                                                    int ncta, const double *__restrict__ partial,
+                                                    double *__restrict__ blk) {
+    __shared__ double S[HQ_NL][NV2];
+    const int lane = threadIdx.x & 31, n = threadIdx.x >> 5;
+    if (n <= N) {
+        double s[NV2];
+#pragma unroll
+        for (int v = 0; v < NV2; v++) s[v] = 0.0;
+        for (int i = lane; i < ncta; i += 32)
+#pragma unroll
+            for (int v = 0; v < NV2; v++) s[v] += partial[((size_t)i * HQ_NL + n) * HQ_NV + v];
+#pragma unroll
+        for (int v = 0; v < NV2; v++) {
+            s[v] = warp_sum(s[v]);
+            if (lane == 0) S[n][v] = s[v];
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    double *lam = blk + V2S_LAM, *mu = blk + V2S_MU, *al = blk + V2S_ALPHA, *be = blk + V2S_BETA;
+    double *pn1 = blk + V2S_PN, *om = blk + V2S_OM, *ka = blk + V2S_KA, *misc = blk + V2S_MISC;
+    if (mode == 2) {
+        double num = 0.0, den = 0.0;
+        for (int L = 0; L <= N; L++) {
+            blk[V2S_RNUM + L] = S[L][V2_RNUM];
+            blk[V2S_RDEN + L] = S[L][V2_RDEN];
+            num += S[L][V2_RNUM];
+            den += S[L][V2_RDEN];
+        }
+        misc[1] = num / den;
+        return;
+    }
+    if (mode == 0) {
+        // init: S = {sum p, sum p mu_m, sum p omega, sum p kappa, sum p lambda_m} over both classes
+        for (int L = 0; L <= N; L++) {
+            lam[L] = S[L][4];
+            mu[L] = S[L][1];
+            om[L] = S[L][2];
+            ka[L] = S[L][3];
+            blk[V2S_SUMP + L] = S[L][0];
+            blk[V2S_DL1 + L] = 0.0;
+        }
+        c = 0;   // the first half-sweep updates class 1
+    } else {
+        for (int L = 1; L <= N - 1; L++) {
+            if (!((active >> L) & 1u)) continue;
+            const double lnew = full_lists ? Lam * S[L][V2_P] : S[L][V2_LAM];
+            const double mstar = al[L] * lam[L - 1];
+            // Eq. muHeter via the exact flow identity sum_m p den = mu* + lambda_old(n)
+            const double mnew = mstar + lam[L] - lnew;
+            blk[V2S_MUSTAR + L] = mstar;
+            lam[L] = lnew;
+            mu[L] = mnew;
+            om[L] = S[L][V2_OM];
+            ka[L] = S[L][V2_KA];
+            blk[V2S_SUMP + L] = S[L][V2_P];
+            blk[V2S_DL1 + L] = S[L][V2_DL1];
+            if (!(S[L][V2_P] > 0.0) || !isfinite(mnew)) misc[0] = 1.0;
+        }
+    }
+    // coefficients for the next half-sweep (class 1 - c)
+    const int nc = 1 - c;
+    for (int L = 1; L <= N - 1; L++) {
+        if ((L & 1) != nc) continue;
+        const double b = lam[L] / mu[L + 1];
+        const double a = (1.0 - b * ka[L + 1]) / om[L - 1];
+        be[L] = b;
+        al[L] = a;
+        if (!(om[L - 1] > 0.0) || !isfinite(a) || !(a > 0.0)) misc[0] = 1.0;
+    }
+    // Eq. bnd_stationary
+    double prod = 1.0, tot = 1.0;
+    double g[HQ_NL];
+    g[0] = 1.0;
+    for (int L = 1; L <= N; L++) {
+        prod *= lam[L - 1] / mu[L];
+        g[L] = prod;
+        tot += prod;
+    }
+    pn1[0] = 0.0;
+    for (int L = 0; L <= N; L++) pn1[L + 1] = g[L] / tot;
+    for (int L = N + 2; L < 34; L++) pn1[L] = 0.0;
+    double prox = 0.0;
+    for (int L = 1; L <= N - 1; L++) prox += pn1[L + 1] * blk[V2S_DL1 + L];
+    misc[2] = prox;
+}
+
+// pi[m_abi] = p(w(m)) p_{w(m)}(m), internal index m -> ABI index via perm.
+__global__ void k_assemble2(int N, const double *__restrict__ pw, const double *__restrict__ pn1, PermArg perm,
+                            double *__restrict__ pi) {
+    const uint64_t S = 1ull << N, half = S >> 1;
+    for (uint64_t m = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; m < S; m += (uint64_t)gridDim.x * blockDim.x) {
+        const int n = __popcll(m);
+        const uint64_t off = (n & 1) ? half : 0;
+        uint64_t ma = 0;
+        for (int u = 0; u < N; u++) ma |= ((m >> u) & 1ull) << perm.p[u];
+        pi[ma] = pn1[n + 1] * pw[off + (m >> 1)];
+    }
+}
+
+}  // namespace hq2
+
+// ---------------------------------------------------------------------------
+namespace hq2_launch {
+
+int sweep_grid(int nsm) { return nsm * 2; }
+
+cudaError_t lambda_states(const P2Args &a, double *lamarr, int grid, cudaStream_t s) {
+    hq2::k_lambda_states<<<grid, 256, 0, s>>>(a, lamarr);
+    return cudaGetLastError();
+}
+cudaError_t omkap(const P2Args &a, const double *lamarr, double2 *ok, int grid, cudaStream_t s) {
+    hq2::k_omkap<<<grid, 256, 0, s>>>(a, lamarr, ok);
+    return cudaGetLastError();
+}
+cudaError_t prog_count(const P2Args &a, const uint32_t *order, uint32_t *size16, int *err, int grid, cudaStream_t s) {
+    hq2::k_prog_count<<<grid, 128, 0, s>>>(a, order, size16, err);
+    return cudaGetLastError();
+}
+cudaError_t prog_scan(const uint32_t *size16, uint32_t *off16, uint64_t n, void *tmp, size_t *tmp_bytes,
+                      cudaStream_t s) {
+    return cub::DeviceScan::ExclusiveSum(tmp, *tmp_bytes, size16, off16, (int)n, s);
+}
+cudaError_t prog_write(const P2Args &a, const uint32_t *order, const uint32_t *off16, uint4 *prog, int grid,
+                       cudaStream_t s) {
+    hq2::k_prog_write<<<grid, 128, 0, s>>>(a, order, off16, prog);
+    return cudaGetLastError();
+}
+cudaError_t sweep(const S2Args &a, int mode, int grid, cudaStream_t s) {
+    if (mode == 0) hq2::k_sweep2<0><<<grid, hq2::WARPS * 32, 0, s>>>(a);
+    else if (mode == 1) hq2::k_sweep2<1><<<grid, hq2::WARPS * 32, 0, s>>>(a);
+    else hq2::k_sweep2<2><<<grid, hq2::WARPS * 32, 0, s>>>(a);
+    return cudaGetLastError();
+}
+cudaError_t scalars(int N, int full_lists, double Lam, int mode, int c, uint32_t active, int ncta,
+                    const double *partial, double *blk, cudaStream_t s) {
+    hq2::k_scalars2<<<1, 1024, 0, s>>>(N, full_lists, Lam, mode, c, active, ncta, partial, blk);
+    return cudaGetLastError();
+}
+cudaError_t assemble(int N, const double *pw, const double *pn1, const int *perm, double *pi, int grid,
+                     cudaStream_t s) {
+    PermArg pa;
+    for (int u = 0; u < 32; u++) pa.p[u] = u < N ? perm[u] : 0;
+    hq2::k_assemble2<<<grid, 256, 0, s>>>(N, pw, pn1, pa, pi);
+    return cudaGetLastError();
+}
+
+}  // namespace hq2_launch

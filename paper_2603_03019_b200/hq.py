@@ -24,7 +24,8 @@ HQ_E_ORDER = -5
 HQ_STATS_LEN = 16
 STATUS_NAMES = {0: "HQ_OK", 1: "HQ_NOT_CONVERGED", -1: "HQ_E_INVAL", -2: "HQ_E_NOMEM", -3: "HQ_E_CUDA",
                 -4: "HQ_E_NUMERIC", -5: "HQ_E_ORDER"}
-EXPORTED = ["hq_create", "hq_solve", "hq_measures", "hq_destroy", "hq_error_string", "hq_stats", "hq_version"]
+EXPORTED = ["hq_create", "hq_solve", "hq_measures", "hq_destroy", "hq_error_string", "hq_stats", "hq_version",
+            "hq_debug_copy"]
 
 _dptr = ctypes.POINTER(ctypes.c_double)
 _lib = None
@@ -62,6 +63,8 @@ def load():
     lib.hq_stats.argtypes = [ctypes.c_void_p, _dptr]
     lib.hq_version.restype = ctypes.c_char_p
     lib.hq_version.argtypes = []
+    lib.hq_debug_copy.restype = ctypes.c_int
+    lib.hq_debug_copy.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t]
     _lib = lib
     return lib
 
@@ -133,6 +136,15 @@ def hq_stats(h):
     return out
 
 
+def hq_debug_copy(h, which, nbytes, dtype):
+    """Copy an internal device array (see include/hq.h) into a numpy array."""
+    out = np.zeros(nbytes // np.dtype(dtype).itemsize, dtype=dtype)
+    st = load().hq_debug_copy(ctypes.c_void_p(h), int(which), out.ctypes.data, out.nbytes)
+    if st != HQ_OK:
+        raise HQError(st, "hq_debug_copy failed")
+    return out
+
+
 def hq_version():
     return load().hq_version().decode()
 
@@ -177,7 +189,7 @@ class Solver:
     def stats(self):
         s = hq_stats(self.h)
         keys = ["sweeps", "halfsweeps", "state_updates", "launches", "residual_evals", "trie_nodes", "sum_pi_minus_1",
-                "solve_ms", "sweep_ms", "sweep_launches", "residual_ms"]
+                "solve_ms", "sweep_ms", "sweep_launches", "residual_ms", "precompute_ms", "program_bytes", "path"]
         return {k: float(s[i]) for i, k in enumerate(keys)}
 
     def close(self):
