@@ -201,6 +201,7 @@ struct hq_problem {
     double *d_lamarr = nullptr;
     double *d_blk = nullptr, *h_blk = nullptr;
     int sgrid = 0;
+    uint32_t total16 = 0, maxrec = 0;
     double prog_bytes = 0.0, precompute_ms = 0.0;
     std::vector<cudaEvent_t> ev;   // per-half-sweep timing events (pairs), reused across solves
 
@@ -508,18 +509,33 @@ static hq_status v2_prepare(hq_problem *h, cudaStream_t s) {
     void *tmp = nullptr;
     HQ_CUDA(alloc(&tmp, tmpb));
     HQ_CUDA(hq2_launch::prog_scan(h->d_size16, h->d_off16, ntiles, tmp, &tmpb, s));
+    uint32_t *d_max = nullptr;
+    HQ_CUDA(alloc((void **)&d_max, 4));
+    size_t tmpb2 = 0;
+    HQ_CUDA(hq2_launch::prog_max(h->d_size16, d_max, ntiles, nullptr, &tmpb2, s));
+    void *tmp2 = nullptr;
+    HQ_CUDA(alloc(&tmp2, tmpb2));
+    HQ_CUDA(hq2_launch::prog_max(h->d_size16, d_max, ntiles, tmp2, &tmpb2, s));
     uint32_t last[2] = {0, 0};
     int herr = 0;
+    HQ_CUDA(cudaMemcpyAsync(&h->maxrec, d_max, 4, cudaMemcpyDeviceToHost, s));
     HQ_CUDA(cudaMemcpyAsync(&last[0], h->d_off16 + ntiles - 1, 4, cudaMemcpyDeviceToHost, s));
     HQ_CUDA(cudaMemcpyAsync(&last[1], h->d_size16 + ntiles - 1, 4, cudaMemcpyDeviceToHost, s));
     HQ_CUDA(cudaMemcpyAsync(&herr, h->d_err, sizeof(int), cudaMemcpyDeviceToHost, s));
     HQ_CUDA(cudaStreamSynchronize(s));
     cudaFree(tmp);
+    cudaFree(tmp2);
+    cudaFree(d_max);
+    if (hq2_launch::sweep_smem(h->maxrec) > 150 * 1024) {
+        h->err = "rate program of a tile exceeds the shared-memory budget";
+        return HQ_E_NUMERIC;
+    }
     if (herr) {
         h->err = "rate program overflow (too many distinct (unit, pattern) pairs in a tile)";
         return HQ_E_NUMERIC;
     }
     const uint64_t total16 = (uint64_t)last[0] + last[1];
+    h->total16 = (uint32_t)total16;
     if (alloc((void **)&h->d_prog, 16 * total16) != cudaSuccess) {
         cudaGetLastError();
         h->err = "device memory for the rate programs could not be allocated";
@@ -606,6 +622,8 @@ static hq_status solve_v2(hq_problem *h, double tol, int max_iter, double *pi, c
     sa.order = h->d_order;
     sa.off16 = h->d_off16;
     sa.prog = h->d_prog;
+    sa.total16 = h->total16;
+    sa.maxrec = h->maxrec;
     sa.coef = h->d_blk;
     sa.partial = h->d_partial;
 

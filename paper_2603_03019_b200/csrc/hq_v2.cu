@@ -159,8 +159,10 @@ __device__ bool tile_walk(const P2Args &a, uint32_t F, double *W0, PairAcc &P) {
             continue;
         }
         const uint32_t Spre = Sst[d - 1];
-        if (!pair_add(P, W0, u, Spre, __ldg(&a.lam_thr[v]))) return false;
         const uint32_t Sme = Spre | (u < PROG_NVARY ? (1u << u) : 0u);
+        // varying units carry their own bit in the pattern, so that a pair only
+        // applies to states in which the unit is busy (W_u is used only there)
+        if (!pair_add(P, W0, u, Sme, __ldg(&a.lam_thr[v]))) return false;
         if (!a.full_lists) {
             const double e = __ldg(&a.lam_end[v]);
             if (e != 0.0 && !pair_add(P, W0, a.N, Sme, e)) return false;
@@ -187,7 +189,7 @@ __global__ void k_prog_count(P2Args a, const uint32_t *__restrict__ order, uint3
         for (int u = 0; u <= HQ_MAXN; u++) cnt[u] = 0;
         for (int k = 0; k < P.n; k++) cnt[P.key[k] & 63]++;
         for (int u = 0; u <= HQ_MAXN; u++)
-            if (cnt[u] > 255) atomicExch(err, 3);
+            if (cnt[u] > 65535) atomicExch(err, 3);
         size16[i] = PROG_HDR16 + (uint32_t)P.n;
     }
 }
@@ -214,14 +216,14 @@ __global__ void k_prog_write(P2Args a, const uint32_t *__restrict__ order, const
             P.key[y + 1] = k;
             P.val[y + 1] = vv;
         }
-        uint32_t cw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        uint32_t cw[16];
+        for (int q = 0; q < 16; q++) cw[q] = 0;
         for (int k = 0; k < P.n; k++) {
             const int u = P.key[k] & 63;
-            cw[u >> 2] += 1u << ((u & 3) * 8);
+            cw[u >> 1] += 1u << ((u & 1) * 16);
         }
-        out[0] = make_uint4(cw[0], cw[1], cw[2], cw[3]);
-        out[1] = make_uint4(cw[4], cw[5], cw[6], cw[7]);
-        double *w0o = reinterpret_cast<double *>(out + 2);
+        for (int q = 0; q < 4; q++) out[q] = make_uint4(cw[4 * q], cw[4 * q + 1], cw[4 * q + 2], cw[4 * q + 3]);
+        double *w0o = reinterpret_cast<double *>(out + PROG_CNT16);
         for (int u = 0; u < 32; u++) w0o[u] = u <= HQ_MAXN ? W0[u] : 0.0;
         for (int k = 0; k < P.n; k++) {
             const uint32_t S = P.key[k] >> 6;
@@ -246,15 +248,23 @@ __global__ void k_prog_write(P2Args a, const uint32_t *__restrict__ order, const
 //   MODE 0: sweep (write p of the active layers of class c)
 //   MODE 1: sweep + per-layer sum |p_new - p_old| (convergence proxy)
 //   MODE 2: residual of Eq. balance_eq_heter for the states of class c
+// NV per-layer values are reduced (sweep: p, p omega, p kappa [, p lambda]
+// [, |dp|]; residual: |out - in|, out).
 // ---------------------------------------------------------------------------
 constexpr int WARPS = 8;
 
-template <int MODE>
-__device__ __forceinline__ void flush_bins(double (&bins)[3][NV2], int K, int c, int pcl, int lane,
-                                           double (*wacc)[NV2]) {
+// acc += a * b if pred != 0 (forced predication: no selects, no branches)
+__device__ __forceinline__ void pfma(double &acc, double a, double b, uint32_t pred) {
+    asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %3, 0;\n\t@p fma.rn.f64 %0, %1, %2, %0;\n\t}"
+        : "+d"(acc) : "d"(a), "d"(b), "r"(pred));
+}
+
+template <int NV>
+__device__ __forceinline__ void flush_bins(double (&bins)[3][NV], int K, int c, int pcl, int lane,
+                                           double (*wacc)[HQ_NV]) {
     if (K < 0) return;
     // bin k of this lane holds layer L_k = K + pcl + k + ((c ^ K ^ pcl ^ k) & 1)
-    const int Lmin = K + ((c ^ K) & 1);   // smallest layer of parity c that can occur
+    const int Lmin = K + ((c ^ K) & 1);
     int Lk[3];
 #pragma unroll
     for (int k = 0; k < 3; k++) Lk[k] = K + pcl + k + ((c ^ K ^ pcl ^ k) & 1);
@@ -264,7 +274,7 @@ __device__ __forceinline__ void flush_bins(double (&bins)[3][NV2], int K, int c,
         const bool any = (Lk[0] == L) || (Lk[1] == L) || (Lk[2] == L);
         if (!__any_sync(0xffffffffu, any)) continue;
 #pragma unroll
-        for (int v = 0; v < NV2; v++) {
+        for (int v = 0; v < NV; v++) {
             double s = 0.0;
 #pragma unroll
             for (int k = 0; k < 3; k++) s += (Lk[k] == L) ? bins[k][v] : 0.0;
@@ -275,23 +285,41 @@ __device__ __forceinline__ void flush_bins(double (&bins)[3][NV2], int K, int c,
 #pragma unroll
     for (int k = 0; k < 3; k++)
 #pragma unroll
-        for (int v = 0; v < NV2; v++) bins[k][v] = 0.0;
+        for (int v = 0; v < NV; v++) bins[k][v] = 0.0;
 }
 
-template <int MODE>
+// apply the pairs of one unit: A_r += c * q_r for the states r the pattern admits
+__device__ __forceinline__ void apply_pairs(const uint4 *__restrict__ my, int &pp, int cnt, uint32_t lane,
+                                            int beta, const double (&q)[4], double (&A)[4]) {
+    const int sh = 8 + 4 * beta;
+    for (int k = 0; k < cnt; k++) {
+        const uint4 rec = my[pp + k];
+        const double cc = __hiloint2double((int)rec.y, (int)rec.x);
+        const uint32_t w = rec.z;
+        const uint32_t m4 = (((w & 31u) & ~lane) == 0u) ? ((w >> sh) & 15u) : 0u;
+        pfma(A[0], cc, q[0], m4 & 1u);
+        pfma(A[1], cc, q[1], m4 & 2u);
+        pfma(A[2], cc, q[2], m4 & 4u);
+        pfma(A[3], cc, q[3], m4 & 8u);
+    }
+    pp += cnt;
+}
+
+template <int MODE, int NV, bool FULL>
 __global__ void __launch_bounds__(WARPS * 32, 2) k_sweep2(S2Args a) {
-    __shared__ double s_x[32];       // alpha(n) (sweep) or p(n-1) (residual, shifted)
+    __shared__ double s_x[32];       // alpha(n) (sweep) or p(n-1) (residual)
     __shared__ double s_y[32];       // beta(n)  (sweep) or p(n+1)
-    __shared__ double s_z[32];       // unused (sweep) or p(n)
-    __shared__ double wacc[WARPS][HQ_NL][NV2];
+    __shared__ double s_z[32];       // p(n) (residual)
+    __shared__ double wacc[WARPS][HQ_NL][HQ_NV];
+    extern __shared__ uint4 sprog[];   // [WARPS][maxrec]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int i = tid; i < WARPS * HQ_NL * NV2; i += blockDim.x) (&wacc[0][0][0])[i] = 0.0;
+    for (int i = tid; i < WARPS * HQ_NL * HQ_NV; i += blockDim.x) (&wacc[0][0][0])[i] = 0.0;
     if (tid < 32) {
         if (MODE == 2) {
             const double *pn1 = a.coef + V2S_PN;   // pn1[n + 1] = p(n)
-            s_x[tid] = pn1[tid];                   // p(n - 1)
-            s_y[tid] = tid + 2 < 34 ? pn1[tid + 2] : 0.0;   // p(n + 1)
-            s_z[tid] = pn1[tid + 1];               // p(n)
+            s_x[tid] = pn1[tid];
+            s_y[tid] = tid + 2 < 34 ? pn1[tid + 2] : 0.0;
+            s_z[tid] = pn1[tid + 1];
         } else {
             s_x[tid] = a.coef[V2S_ALPHA + tid];
             s_y[tid] = a.coef[V2S_BETA + tid];
@@ -299,6 +327,9 @@ __global__ void __launch_bounds__(WARPS * 32, 2) k_sweep2(S2Args a) {
         }
     }
     __syncthreads();
+    uint4 *__restrict__ my = sprog + (size_t)warp * a.maxrec;
+    const uint16_t *__restrict__ mycnt = reinterpret_cast<const uint16_t *>(my);
+    const double *__restrict__ myw0 = reinterpret_cast<const double *>(my + PROG_CNT16);
 
     const int pcl = __popc(lane);
     const uint64_t nwarps = (uint64_t)gridDim.x * WARPS;
@@ -306,31 +337,27 @@ __global__ void __launch_bounds__(WARPS * 32, 2) k_sweep2(S2Args a) {
     const uint64_t chunk = (a.ntiles + nwarps - 1) / nwarps;
     const uint64_t i0 = gw * chunk;
     const uint64_t i1 = min(i0 + chunk, a.ntiles);
-    const uint32_t fullm = (a.N >= 32) ? 0xffffffffu : ((1u << a.N) - 1u);
+    const uint32_t fullm = (1u << a.N) - 1u;
+    const uint32_t ulane = (uint32_t)lane;
 
-    // per-lane constants: service rate of the lane units (1..5) that are busy
     double mu_lane = 0.0;
 #pragma unroll
     for (int b = 0; b < 5; b++)
         if ((lane >> b) & 1) mu_lane += a.nu[1 + b];
 
-    double bins[3][NV2];
+    double bins[3][NV];
 #pragma unroll
     for (int k = 0; k < 3; k++)
 #pragma unroll
-        for (int v = 0; v < NV2; v++) bins[k][v] = 0.0;
+        for (int v = 0; v < NV; v++) bins[k][v] = 0.0;
     int curK = -1;
+    const double *__restrict__ Q = a.Q;
 
     for (uint64_t i = i0; i < i1; i++) {
         const uint32_t t = __ldg(a.order + i);
         const int K = __popc(t);
-        if (K != curK) {
-            flush_bins<MODE>(bins, curK, a.c, pcl, lane, wacc[warp]);
-            curK = K;
-        }
         const uint32_t jb = t << PROG_TB;
-        const int beta = (a.c ^ K ^ pcl) & 1;
-        const double *__restrict__ Q = a.Q;
+        // issue the tile's global loads first: own-index neighbours, old p, scatter weights, program
         double qo[4];
 #pragma unroll
         for (int r = 0; r < 4; r++) qo[r] = __ldg(Q + jb + r * 32 + lane);
@@ -339,95 +366,92 @@ __global__ void __launch_bounds__(WARPS * 32, 2) k_sweep2(S2Args a) {
 #pragma unroll
             for (int r = 0; r < 4; r++) pold[r] = a.P[jb + r * 32 + lane];
         }
-        const uint4 *__restrict__ pg = a.prog + __ldg(a.off16 + i);
-        const uint4 h0 = __ldg(pg), h1 = __ldg(pg + 1);
-        const uint32_t cw[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
-        const double *__restrict__ w0 = reinterpret_cast<const double *>(pg + 2);
+        const uint32_t o = __ldg(a.off16 + i);
+        const uint32_t nrec = ((i + 1 < a.ntiles) ? __ldg(a.off16 + i + 1) : a.total16) - o;
+        __syncwarp();
+        for (uint32_t k = lane; k < nrec; k += 32) my[k] = __ldg(a.prog + o + k);
+        if (K != curK) {
+            flush_bins<NV>(bins, curK, a.c, pcl, lane, wacc[warp]);
+            curK = K;
+        }
+        __syncwarp();
+        const int beta = (a.c ^ K ^ pcl) & 1;
         int pp = PROG_HDR16;
         double A[4] = {0.0, 0.0, 0.0, 0.0}, D[4] = {0.0, 0.0, 0.0, 0.0};
         double mu_fix = 0.0;
-
+        // ---- varying units 0..7 (per-state busy status)
+        {   // unit 0: the implied parity bit; busy in state r iff beta ^ parity(r)
+            const double nu = a.nu[0];
+            const uint32_t fr0 = (uint32_t)(beta ^ 1), fr1 = (uint32_t)beta;   // free in r with parity 0 / 1
+            pfma(D[0], nu, qo[0], fr0);
+            pfma(D[1], nu, qo[1], fr1);
+            pfma(D[2], nu, qo[2], fr1);
+            pfma(D[3], nu, qo[3], fr0);
+            apply_pairs(my, pp, mycnt[0], ulane, beta, qo, A);
+        }
 #pragma unroll
-        for (int u = 0; u < HQ_MAXN; u++) {
-            if (u >= a.N) break;
-            const int cnt = (int)((cw[u >> 2] >> ((u & 3) * 8)) & 0xffu);
-            const bool fixed = u >= PROG_NVARY;
-            const bool fbusy = fixed && ((t >> (u - PROG_NVARY)) & 1u);
+        for (int u = 1; u <= 5; u++) {
             double q[4];
-            if (u == 0) {
 #pragma unroll
-                for (int r = 0; r < 4; r++) q[r] = qo[r];
-            } else if (u <= 5) {
+            for (int r = 0; r < 4; r++) q[r] = __shfl_xor_sync(0xffffffffu, qo[r], 1 << (u - 1));
+            const double nu = a.nu[u];
+            const uint32_t fr = ((lane >> (u - 1)) & 1) ^ 1;
 #pragma unroll
-                for (int r = 0; r < 4; r++) q[r] = __shfl_xor_sync(0xffffffffu, qo[r], 1 << (u - 1));
-            } else if (u <= 7) {
+            for (int r = 0; r < 4; r++) pfma(D[r], nu, q[r], fr);
+            apply_pairs(my, pp, mycnt[u], ulane, beta, q, A);
+        }
 #pragma unroll
-                for (int r = 0; r < 4; r++) q[r] = qo[r ^ (1 << (u - 6))];
-            } else {
-                const double *__restrict__ qn = Q + (jb ^ (1u << (u - 1))) + lane;
+        for (int u = 6; u <= 7; u++) {
+            double q[4];
 #pragma unroll
-                for (int r = 0; r < 4; r++) q[r] = __ldg(qn + r * 32);
+            for (int r = 0; r < 4; r++) q[r] = qo[r ^ (1 << (u - 6))];
+            const double nu = a.nu[u];
+#pragma unroll
+            for (int r = 0; r < 4; r++)
+                if (!((r >> (u - 6)) & 1)) D[r] = fma(nu, q[r], D[r]);
+            apply_pairs(my, pp, mycnt[u], ulane, beta, q, A);
+        }
+        // ---- fixed units 8..N-1 (tile-uniform busy status), one unit of prefetch
+        double qn[4];
+        {
+            const double *__restrict__ qp = Q + (jb ^ (1u << 7)) + lane;
+#pragma unroll
+            for (int r = 0; r < 4; r++) qn[r] = (a.N > 8) ? __ldg(qp + r * 32) : 0.0;
+        }
+#pragma unroll
+        for (int u = 8; u < HQ_MAXN; u++) {
+            if (u >= a.N) break;
+            double q[4];
+#pragma unroll
+            for (int r = 0; r < 4; r++) q[r] = qn[r];
+            if (u + 1 < a.N) {
+                const double *__restrict__ qp = Q + (jb ^ (1u << u)) + lane;
+#pragma unroll
+                for (int r = 0; r < 4; r++) qn[r] = __ldg(qp + r * 32);
             }
             const double nu = a.nu[u];
-            if (fixed && !fbusy) {
+            if (!((t >> (u - PROG_NVARY)) & 1u)) {
 #pragma unroll
                 for (int r = 0; r < 4; r++) D[r] = fma(nu, q[r], D[r]);
                 continue;
             }
-            double W[4];
-            const double wu = __ldg(w0 + u);
+            mu_fix += nu;
+            const double w0 = myw0[u];
 #pragma unroll
-            for (int r = 0; r < 4; r++) W[r] = wu;
-            for (int k = 0; k < cnt; k++) {
-                const uint4 rec = __ldg(pg + pp + k);
-                const double cc = __hiloint2double((int)rec.y, (int)rec.x);
-                const uint32_t w = rec.z;
-                const bool tl = ((w & 31u) & ~(uint32_t)lane) == 0u;
-                const uint32_t m4 = tl ? ((w >> (8 + 4 * beta)) & 15u) : 0u;
-#pragma unroll
-                for (int r = 0; r < 4; r++)
-                    if ((m4 >> r) & 1u) W[r] += cc;
-            }
-            pp += cnt;
-            if (fixed) {
-                mu_fix += nu;
-#pragma unroll
-                for (int r = 0; r < 4; r++) A[r] = fma(W[r], q[r], A[r]);
-            } else {
-#pragma unroll
-                for (int r = 0; r < 4; r++) {
-                    const int b0r = beta ^ (__popc(r) & 1);
-                    const bool busy = (u == 0) ? (b0r != 0) : (u <= 5) ? (((lane >> (u - 1)) & 1) != 0)
-                                                                       : (((r >> (u - 6)) & 1) != 0);
-                    if (busy) A[r] = fma(W[r], q[r], A[r]);
-                    else D[r] = fma(nu, q[r], D[r]);
-                }
-            }
+            for (int r = 0; r < 4; r++) A[r] = fma(w0, q[r], A[r]);
+            apply_pairs(my, pp, mycnt[u], ulane, beta, q, A);
         }
-        // blocked pseudo-unit (truncated lists): lambda_m = Lambda - blocked
+        // ---- lambda_m (blocked pseudo-unit for truncated lists)
         double lam[4];
-        if (a.full_lists) {
+        if (FULL) {
 #pragma unroll
             for (int r = 0; r < 4; r++) lam[r] = a.Lam;
         } else {
             const int u = a.N;
-            uint32_t word = 0;
-#pragma unroll
-            for (int q = 0; q < 8; q++)
-                if (q == (u >> 2)) word = cw[q];
-            const int cnt = (int)((word >> ((u & 3) * 8)) & 0xffu);
-            const double wu = __ldg(w0 + u);
-            double Bk[4] = {wu, wu, wu, wu};
-            for (int k = 0; k < cnt; k++) {
-                const uint4 rec = __ldg(pg + pp + k);
-                const double cc = __hiloint2double((int)rec.y, (int)rec.x);
-                const uint32_t w = rec.z;
-                const bool tl = ((w & 31u) & ~(uint32_t)lane) == 0u;
-                const uint32_t m4 = tl ? ((w >> (8 + 4 * beta)) & 15u) : 0u;
-#pragma unroll
-                for (int r = 0; r < 4; r++)
-                    if ((m4 >> r) & 1u) Bk[r] += cc;
-            }
+            const double w0 = myw0[u];
+            double Bk[4] = {w0, w0, w0, w0};
+            const double one[4] = {1.0, 1.0, 1.0, 1.0};
+            apply_pairs(my, pp, mycnt[u], ulane, beta, one, Bk);
 #pragma unroll
             for (int r = 0; r < 4; r++) lam[r] = a.Lam - Bk[r];
         }
@@ -438,37 +462,48 @@ __global__ void __launch_bounds__(WARPS * 32, 2) k_sweep2(S2Args a) {
             const int b0r = beta ^ (pr & 1);
             const int n = K + pcl + pr + b0r;
             const uint32_t j = jb + r * 32 + lane;
-            double mu = mu_fix + mu_lane + (b0r ? a.nu[0] : 0.0) + ((r & 1) ? a.nu[6] : 0.0) + ((r & 2) ? a.nu[7] : 0.0);
+            const double mu = mu_fix + mu_lane + (b0r ? a.nu[0] : 0.0) + ((r & 1) ? a.nu[6] : 0.0) +
+                              ((r & 2) ? a.nu[7] : 0.0);
             double lm = lam[r];
-            if (a.full_lists && ((((j << 1) | (uint32_t)b0r)) == fullm)) lm = 0.0;
+            if (FULL && (((j << 1) | (uint32_t)b0r) == fullm)) lm = 0.0;
             const double den = lm + mu;
-            const double rden = __drcp_rn(den);
             if (MODE == 2) {
                 const double out = s_z[n] * pold[r] * den;
                 const double in = s_x[n] * A[r] + s_y[n] * D[r];
-                bins[pr][V2_RNUM] += fabs(out - in);
-                bins[pr][V2_RDEN] += out;
+                bins[pr][0] += fabs(out - in);
+                bins[pr][1] += out;
             } else {
                 if (!((a.active >> n) & 1u)) continue;
+                const double rden = __drcp_rn(den);
                 const double p = (s_x[n] * A[r] + s_y[n] * D[r]) * rden;
                 a.P[j] = p;
                 const double2 ok = __ldg(okp + j);
-                bins[pr][V2_P] += p;
-                bins[pr][V2_OM] += p * ok.x;
-                bins[pr][V2_KA] += p * ok.y;
-                bins[pr][V2_LAM] += p * lm;
-                if (MODE == 1) bins[pr][V2_DL1] += fabs(p - pold[r]);
+                bins[pr][0] += p;
+                bins[pr][1] += p * ok.x;
+                bins[pr][2] += p * ok.y;
+                if (!FULL) bins[pr][3] += p * lm;
+                if (MODE == 1) bins[pr][NV - 1] += fabs(p - pold[r]);
             }
         }
     }
-    flush_bins<MODE>(bins, curK, a.c, pcl, lane, wacc[warp]);
+    flush_bins<NV>(bins, curK, a.c, pcl, lane, wacc[warp]);
     __syncthreads();
+    // map the kernel's value slots onto the reduction layout V2_*
     double *out = a.partial + (size_t)blockIdx.x * HQ_NL * HQ_NV;
-    for (int i = tid; i < HQ_NL * NV2; i += blockDim.x) {
-        const int L = i / NV2, v = i % NV2;
+    for (int i = tid; i < HQ_NL * HQ_NV; i += blockDim.x) {
+        const int L = i / HQ_NV, v = i % HQ_NV;
         double s = 0.0;
+        int src = -1;
+        if (MODE == 2) src = (v < 2) ? v : -1;
+        else if (v == V2_P) src = 0;
+        else if (v == V2_OM) src = 1;
+        else if (v == V2_KA) src = 2;
+        else if (v == V2_LAM) src = FULL ? -1 : 3;
+        else if (v == V2_DL1) src = (MODE == 1) ? NV - 1 : -1;
+        if (src >= 0) {
 #pragma unroll
-        for (int w = 0; w < WARPS; w++) s += wacc[w][L][v];
+            for (int w = 0; w < WARPS; w++) s += wacc[w][L][src];
+        }
         out[L * HQ_NV + v] = s;
     }
 }
@@ -590,6 +625,7 @@ namespace hq2_launch {
 
 int sweep_grid(int nsm) { return nsm * 2; }
 
+
 cudaError_t lambda_states(const P2Args &a, double *lamarr, int grid, cudaStream_t s) {
     hq2::k_lambda_states<<<grid, 256, 0, s>>>(a, lamarr);
     return cudaGetLastError();
@@ -611,11 +647,33 @@ cudaError_t prog_write(const P2Args &a, const uint32_t *order, const uint32_t *o
     hq2::k_prog_write<<<grid, 128, 0, s>>>(a, order, off16, prog);
     return cudaGetLastError();
 }
-cudaError_t sweep(const S2Args &a, int mode, int grid, cudaStream_t s) {
-    if (mode == 0) hq2::k_sweep2<0><<<grid, hq2::WARPS * 32, 0, s>>>(a);
-    else if (mode == 1) hq2::k_sweep2<1><<<grid, hq2::WARPS * 32, 0, s>>>(a);
-    else hq2::k_sweep2<2><<<grid, hq2::WARPS * 32, 0, s>>>(a);
+size_t sweep_smem(uint32_t maxrec) { return sizeof(uint4) * (size_t)maxrec * hq2::WARPS; }
+
+template <int MODE, int NV, bool FULL>
+static cudaError_t launch_sweep(const S2Args &a, int grid, cudaStream_t s) {
+    const size_t sm = sweep_smem(a.maxrec);
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(hq2::k_sweep2<MODE, NV, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+        attr_set = true;
+    }
+    hq2::k_sweep2<MODE, NV, FULL><<<grid, hq2::WARPS * 32, sm, s>>>(a);
     return cudaGetLastError();
+}
+
+cudaError_t sweep(const S2Args &a, int mode, int grid, cudaStream_t s) {
+    if (a.full_lists) {
+        if (mode == 0) return launch_sweep<0, 3, true>(a, grid, s);
+        if (mode == 1) return launch_sweep<1, 4, true>(a, grid, s);
+        return launch_sweep<2, 2, true>(a, grid, s);
+    }
+    if (mode == 0) return launch_sweep<0, 4, false>(a, grid, s);
+    if (mode == 1) return launch_sweep<1, 5, false>(a, grid, s);
+    return launch_sweep<2, 2, false>(a, grid, s);
+}
+
+cudaError_t prog_max(const uint32_t *size16, uint32_t *out, uint64_t n, void *tmp, size_t *tmp_bytes, cudaStream_t s) {
+    return cub::DeviceReduce::Max(tmp, *tmp_bytes, size16, out, (int)n, s);
 }
 cudaError_t scalars(int N, int full_lists, double Lam, int mode, int c, uint32_t active, int ncta,
                     const double *partial, double *blk, cudaStream_t s) {

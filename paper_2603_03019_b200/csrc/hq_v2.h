@@ -9,12 +9,15 @@
 #define PROG_TB 7
 #define PROG_TILE 128
 #define PROG_NVARY 8
-// Program record (16-byte units): [0..1] per-unit pair counts (u8 x 32),
-// [2..17] W0[32] (fp64), then pairs {c: fp64, w: u32, pad} sorted by unit.
-// Unit index N is the "blocked" pseudo-unit (truncated lists): sum of lambda_j
-// over atoms whose whole list is busy.
-#define PROG_HDR16 18
-#define PROG_MAXPAIRS 480
+// Program record (16-byte units): [0..3] per-unit pair counts (u16 x 32),
+// [4..19] W0[32] (fp64; zero for the varying units 0..7, whose contributions
+// are all pairs carrying the unit's own bit), then pairs
+// {c: fp64, w: u32 = lane5 | rm(beta=0) << 8 | rm(beta=1) << 12 | unit << 16, pad}
+// sorted by unit.  Unit index N is the "blocked" pseudo-unit (truncated
+// lists): sum of lambda_j over atoms whose whole list is busy.
+#define PROG_CNT16 4
+#define PROG_HDR16 20
+#define PROG_MAXPAIRS 1024
 
 // per-layer values reduced by the sweep kernel
 #define NV2 5
@@ -48,6 +51,8 @@ struct S2Args {   // sweep / residual kernel
     const uint32_t *order;   // tile visit order (by popcount)
     const uint32_t *off16;   // program offsets (16-byte units), in visit order
     const uint4 *prog;
+    uint32_t total16;        // program buffer size (16-byte units)
+    uint32_t maxrec;         // largest program (16-byte units) = per-warp smem slot
     const double *Q;         // neighbour class
     double *P;               // updated class
     const double2 *omkap;    // scatter weights of the updated class
@@ -82,6 +87,8 @@ cudaError_t prog_scan(const uint32_t *size16, uint32_t *off16, uint64_t n, void 
 cudaError_t prog_write(const P2Args &a, const uint32_t *order, const uint32_t *off16, uint4 *prog, int grid,
                        cudaStream_t s);
 cudaError_t sweep(const S2Args &a, int mode, int grid, cudaStream_t s);
+cudaError_t prog_max(const uint32_t *size16, uint32_t *out, uint64_t n, void *tmp, size_t *tmp_bytes, cudaStream_t s);
+size_t sweep_smem(uint32_t maxrec);
 cudaError_t scalars(int N, int full_lists, double Lam, int mode, int c, uint32_t active, int ncta,
                     const double *partial, double *blk, cudaStream_t s);
 cudaError_t assemble(int N, const double *pw, const double *pn1, const int *perm, double *pi, int grid,

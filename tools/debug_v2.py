@@ -69,10 +69,10 @@ prog = hq.hq_debug_copy(s.h, 3, 16 * total16, np.uint32).reshape(-1, 4)
 maxerr = 0.0
 for i in range(nt):
     t = int(order[i]); o = int(off[i])
-    cw = prog[o:o + 2].reshape(-1)
-    cnt = [(int(cw[u >> 2]) >> ((u & 3) * 8)) & 0xff for u in range(32)]
-    w0 = prog[o + 2:o + 18].reshape(-1).view(np.float64)
-    pp = o + 18
+    cw = prog[o:o + 4].reshape(-1)
+    cnt = [(int(cw[u >> 1]) >> ((u & 1) * 16)) & 0xffff for u in range(32)]
+    w0 = prog[o + 4:o + 20].reshape(-1).view(np.float64)
+    pp = o + 20
     pairs = {}
     for u in range(N + 1):
         pairs[u] = []
