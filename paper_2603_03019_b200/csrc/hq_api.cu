@@ -143,23 +143,67 @@ std::vector<int> choose_perm(int N, const TrieHost &tr) {
     for (int u = 0; u < N; u++) perm[u] = u;
     const char *env = getenv("HQ_PERM");
     if (N < 8 || (env && std::string(env) == "identity")) return perm;
+    // prefix counts: trie nodes with the unit strictly above them on the path
     std::vector<long> cnt(N, 0);
-    std::vector<int> stk;   // units on the current path (preorder + depth)
+    std::vector<int> stk;
+    std::vector<uint32_t> path(tr.node.size()), pre(tr.node.size());
+    std::vector<uint32_t> pstk;
     for (size_t v = 0; v < tr.node.size(); v++) {
         const int u = tr.node[v].x & 0xff, d = (tr.node[v].x >> 8) & 0xff;
         stk.resize(d - 1);
+        pstk.resize(d - 1);
         for (int a : stk) cnt[a]++;
+        pre[v] = d >= 2 ? pstk[d - 2] : 0u;
+        path[v] = pre[v] | (1u << u);
         stk.push_back(u);
+        pstk.push_back(path[v]);
     }
     std::vector<int> idx(N);
     for (int u = 0; u < N; u++) idx[u] = u;
     std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return cnt[a] < cnt[b]; });
+    std::vector<int> L8(idx.begin(), idx.begin() + 8);
+    uint32_t vmask = 0;
+    for (int x : L8) vmask |= 1u << x;
+    // Expected per-state cost of the rate pairs over uniformly random tiles for
+    // a choice of the three register-state units T (internal 0, 6, 7): a node
+    // survives with probability 2^-(fixed units on its path); it costs a
+    // lane-only pair (~1.25 instr/state) or a register-state pair (~4.5).
+    double best = 1e300;
+    int bt[3] = {L8[0], L8[1], L8[2]};
+    for (int a1 = 0; a1 < 8; a1++)
+        for (int a2 = a1 + 1; a2 < 8; a2++)
+            for (int a3 = a2 + 1; a3 < 8; a3++) {
+                const uint32_t T = (1u << L8[a1]) | (1u << L8[a2]) | (1u << L8[a3]);
+                const uint32_t lanes = vmask & ~T;
+                double cost = 0.0;
+                for (size_t v = 0; v < tr.node.size(); v++) {
+                    const int u = tr.node[v].x & 0xff;
+                    const int f = __builtin_popcount(path[v] & ~vmask);
+                    const double w = std::ldexp(1.0, -f);
+                    uint32_t S = pre[v] & vmask;
+                    if ((lanes >> u) & 1u) S |= 1u << u;
+                    if (!S) continue;
+                    cost += (S & T) ? 4.5 * w : 1.25 * w;
+                }
+                if (cost < best) {
+                    best = cost;
+                    bt[0] = L8[a1];
+                    bt[1] = L8[a2];
+                    bt[2] = L8[a3];
+                }
+            }
     std::vector<char> used(N, 0);
-    for (int i = 0; i < 8; i++) {
-        perm[i] = idx[i];
-        used[idx[i]] = 1;
-    }
-    int k = 8;
+    perm[0] = bt[0];
+    perm[6] = bt[1];
+    perm[7] = bt[2];
+    for (int q = 0; q < 3; q++) used[bt[q]] = 1;
+    int k = 1;
+    for (int x : L8)
+        if (!used[x]) {
+            perm[k++] = x;
+            used[x] = 1;
+        }
+    k = 8;
     for (int u = 0; u < N; u++)
         if (!used[u]) perm[k++] = u;
     return perm;

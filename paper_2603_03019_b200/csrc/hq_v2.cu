@@ -160,9 +160,11 @@ __device__ bool tile_walk(const P2Args &a, uint32_t F, double *W0, PairAcc &P) {
         }
         const uint32_t Spre = Sst[d - 1];
         const uint32_t Sme = Spre | (u < PROG_NVARY ? (1u << u) : 0u);
-        // varying units carry their own bit in the pattern, so that a pair only
-        // applies to states in which the unit is busy (W_u is used only there)
-        if (!pair_add(P, W0, u, Sme, __ldg(&a.lam_thr[v]))) return false;
+        // lane units (1..5) carry their own bit in the pattern, so that their
+        // pairs only apply to lanes in which the unit is busy; units 0, 6, 7
+        // get their own-busy condition from the register-state masks.
+        const uint32_t Sp = (u >= 1 && u <= 5) ? Sme : Spre;
+        if (!pair_add(P, W0, u, Sp, __ldg(&a.lam_thr[v]))) return false;
         if (!a.full_lists) {
             const double e = __ldg(&a.lam_end[v]);
             if (e != 0.0 && !pair_add(P, W0, a.N, Sme, e)) return false;
@@ -189,7 +191,7 @@ __global__ void k_prog_count(P2Args a, const uint32_t *__restrict__ order, uint3
         for (int u = 0; u <= HQ_MAXN; u++) cnt[u] = 0;
         for (int k = 0; k < P.n; k++) cnt[P.key[k] & 63]++;
         for (int u = 0; u <= HQ_MAXN; u++)
-            if (cnt[u] > 65535) atomicExch(err, 3);
+            if (cnt[u] > 32767) atomicExch(err, 3);
         size16[i] = PROG_HDR16 + (uint32_t)P.n;
     }
 }
@@ -203,12 +205,15 @@ __global__ void k_prog_write(P2Args a, const uint32_t *__restrict__ order, const
         const uint32_t t = order[i];
         uint4 *out = prog + off16[i];
         if (!tile_walk(a, t << 8, W0, P)) continue;
-        // stable sort of the pairs by unit (insertion sort, DFS order kept within a unit)
+        // stable sort of the pairs by (unit, class): class 0 = lane-only pattern
+        // (no bit of units 0, 6, 7), class 1 = depends on the register state
+        auto cls = [](uint16_t key) -> int { return (((key >> 6) & 0xC1u) != 0u) ? 1 : 0; };
         for (int x = 1; x < P.n; x++) {
             const uint16_t k = P.key[x];
             const double vv = P.val[x];
+            const int kk = (k & 63) * 2 + cls(k);
             int y = x - 1;
-            while (y >= 0 && (P.key[y] & 63) > (k & 63)) {
+            while (y >= 0 && ((P.key[y] & 63) * 2 + cls(P.key[y])) > kk) {
                 P.key[y + 1] = P.key[y];
                 P.val[y + 1] = P.val[y];
                 y--;
@@ -216,13 +221,13 @@ __global__ void k_prog_write(P2Args a, const uint32_t *__restrict__ order, const
             P.key[y + 1] = k;
             P.val[y + 1] = vv;
         }
-        uint32_t cw[16];
-        for (int q = 0; q < 16; q++) cw[q] = 0;
+        uint32_t cw[32];
+        for (int q = 0; q < 32; q++) cw[q] = 0;
         for (int k = 0; k < P.n; k++) {
             const int u = P.key[k] & 63;
-            cw[u >> 1] += 1u << ((u & 1) * 16);
+            cw[u] += cls(P.key[k]) ? (1u << 16) : 1u;   // low half: lane-only count, high half: per-r count
         }
-        for (int q = 0; q < 4; q++) out[q] = make_uint4(cw[4 * q], cw[4 * q + 1], cw[4 * q + 2], cw[4 * q + 3]);
+        for (int q = 0; q < 8; q++) out[q] = make_uint4(cw[4 * q], cw[4 * q + 1], cw[4 * q + 2], cw[4 * q + 3]);
         double *w0o = reinterpret_cast<double *>(out + PROG_CNT16);
         for (int u = 0; u < 32; u++) w0o[u] = u <= HQ_MAXN ? W0[u] : 0.0;
         for (int k = 0; k < P.n; k++) {
@@ -233,7 +238,9 @@ __global__ void k_prog_write(P2Args a, const uint32_t *__restrict__ order, const
             for (int beta = 0; beta < 2; beta++)
                 for (int r = 0; r < 4; r++) {
                     const uint32_t b0 = (uint32_t)beta ^ (uint32_t)(__popc(r) & 1);
-                    if ((sreg & ~(uint32_t)r) == 0 && (!s0 || b0)) rm[beta] |= 1u << r;
+                    // own-busy condition of the register-state units (W_u is used only where u is busy)
+                    const bool own = (u == 0) ? (b0 != 0) : (u == 6) ? ((r & 1) != 0) : (u == 7) ? ((r & 2) != 0) : true;
+                    if ((sreg & ~(uint32_t)r) == 0 && (!s0 || b0) && own) rm[beta] |= 1u << r;
                 }
             const uint32_t w = slane | (rm[0] << 8) | (rm[1] << 12) | ((uint32_t)u << 16);
             const double c = P.val[k];
@@ -288,12 +295,24 @@ __device__ __forceinline__ void flush_bins(double (&bins)[3][NV], int K, int c, 
         for (int v = 0; v < NV; v++) bins[k][v] = 0.0;
 }
 
-// apply the pairs of one unit: A_r += c * q_r for the states r the pattern admits
-__device__ __forceinline__ void apply_pairs(const uint4 *__restrict__ my, int &pp, int cnt, uint32_t lane,
-                                            int beta, const double (&q)[4], double (&A)[4]) {
+// lane-only pairs of one unit: Wt += c if the pattern's lane bits are busy in this lane
+__device__ __forceinline__ double lane_pairs(const uint4 *__restrict__ my, int &pp, int cnt, uint32_t lane, double Wt) {
+    for (int k = 0; k < cnt; k++) {
+        const uint4 rec = __ldg(my + pp + k);
+        const double cc = __hiloint2double((int)rec.y, (int)rec.x);
+        const bool tl = ((rec.z & 31u) & ~lane) == 0u;
+        Wt += tl ? cc : 0.0;
+    }
+    pp += cnt;
+    return Wt;
+}
+
+// register-state pairs of one unit: A_r += c * q_r for the states r the pattern admits
+__device__ __forceinline__ void reg_pairs(const uint4 *__restrict__ my, int &pp, int cnt, uint32_t lane, int beta,
+                                          const double (&q)[4], double (&A)[4]) {
     const int sh = 8 + 4 * beta;
     for (int k = 0; k < cnt; k++) {
-        const uint4 rec = my[pp + k];
+        const uint4 rec = __ldg(my + pp + k);
         const double cc = __hiloint2double((int)rec.y, (int)rec.x);
         const uint32_t w = rec.z;
         const uint32_t m4 = (((w & 31u) & ~lane) == 0u) ? ((w >> sh) & 15u) : 0u;
@@ -305,14 +324,90 @@ __device__ __forceinline__ void apply_pairs(const uint4 *__restrict__ my, int &p
     pp += cnt;
 }
 
+// uniform (REDUX) copy of a warp-uniform value: lets ptxas use uniform branches
+__device__ __forceinline__ int wuni(int x) { return (int)__reduce_max_sync(0xffffffffu, (unsigned)x); }
+
+// streaming load that does not allocate in L1 (L1 is kept for the rate programs)
+__device__ __forceinline__ double ld_stream(const double *p) {
+    double v;
+    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+
+// prefetch the rate program of visit index i into L1 (one 128-byte line per lane)
+__device__ __forceinline__ void prefetch_prog(const S2Args &a, uint64_t i, int lane) {
+    if (i >= a.ntiles) return;
+    const uint32_t o = __ldg(a.off16 + i);
+    const uint32_t nrec = ((i + 1 < a.ntiles) ? __ldg(a.off16 + i + 1) : a.total16) - o;
+    const char *base = reinterpret_cast<const char *>(a.prog + o);
+    const uint32_t nlines = (nrec * 16 + 127) / 128 + 1;
+    for (uint32_t k = lane; k < nlines; k += 32)
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(base + 128 * (size_t)k));
+}
+
+// ---------------------------------------------------------------------------
+// Per-warp TMA ring.  Every operand block of a tile (128 doubles = 1 KB:
+// the own-index neighbours, the old p, the N-8 fixed-unit neighbour blocks,
+// and the two halves of the scatter weights) is bulk-copied (cp.async.bulk,
+// completion on an mbarrier) into a ring of RING slots; lanes 0..G-1 issue
+// G blocks at once whenever G slots are free, so the copies run RING-G
+// blocks ahead of the consumer without occupying registers.
+// ---------------------------------------------------------------------------
+constexpr int RING = 8;
+constexpr int G = 4;
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count));
+}
+__device__ __forceinline__ void tma_load_1k(void *dst, const void *src, uint64_t *bar) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], 1024;" ::"r"(b) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 1024, [%2];"
+                 ::"r"(d), "l"(src), "r"(b) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n\t}" ::"r"(b), "r"(parity) : "memory");
+}
+
+template <int MODE>
+struct Stream {
+    // block layout of one tile: [qown][pold?][nbr 8..N-1][omk lo, omk hi]?
+    int nb;          // blocks per tile
+    int nfix;        // N - 8
+    __device__ __forceinline__ void init(int N) {
+        nfix = N - PROG_NVARY;
+        nb = 1 + (MODE >= 1 ? 1 : 0) + nfix + (MODE < 2 ? 2 : 0);
+    }
+    // source address of block b of the tile with index t
+    __device__ __forceinline__ const void *src(const S2Args &a, uint32_t t, int b) const {
+        const uint32_t jb = t << PROG_TB;
+        int x = b;
+        if (x == 0) return a.Q + jb;
+        x--;
+        if (MODE >= 1) {
+            if (x == 0) return a.P + jb;
+            x--;
+        }
+        if (x < nfix) return a.Q + (jb ^ (1u << (PROG_NVARY - 1 + x)));
+        x -= nfix;
+        return a.omkap + jb + 64 * x;
+    }
+};
+
 template <int MODE, int NV, bool FULL>
 __global__ void __launch_bounds__(WARPS * 32, 2) k_sweep2(S2Args a) {
     __shared__ double s_x[32];       // alpha(n) (sweep) or p(n-1) (residual)
     __shared__ double s_y[32];       // beta(n)  (sweep) or p(n+1)
     __shared__ double s_z[32];       // p(n) (residual)
     __shared__ double wacc[WARPS][HQ_NL][HQ_NV];
-    extern __shared__ uint4 sprog[];   // [WARPS][maxrec]
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    __shared__ uint64_t sbar[WARPS][RING];
+    extern __shared__ __align__(128) double sring[];   // [WARPS][RING][128]
+    const int tid = threadIdx.x, lane = tid & 31, warp = wuni(threadIdx.x >> 5);
     for (int i = tid; i < WARPS * HQ_NL * HQ_NV; i += blockDim.x) (&wacc[0][0][0])[i] = 0.0;
     if (tid < 32) {
         if (MODE == 2) {
@@ -326,10 +421,11 @@ __global__ void __launch_bounds__(WARPS * 32, 2) k_sweep2(S2Args a) {
             s_z[tid] = 0.0;
         }
     }
+    if (lane < RING) mbar_init(&sbar[warp][lane], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();
-    uint4 *__restrict__ my = sprog + (size_t)warp * a.maxrec;
-    const uint16_t *__restrict__ mycnt = reinterpret_cast<const uint16_t *>(my);
-    const double *__restrict__ myw0 = reinterpret_cast<const double *>(my + PROG_CNT16);
+    double *__restrict__ ring = sring + (size_t)warp * RING * 128;
+    uint64_t *bars = sbar[warp];
 
     const int pcl = __popc(lane);
     const uint64_t nwarps = (uint64_t)gridDim.x * WARPS;
@@ -337,8 +433,53 @@ __global__ void __launch_bounds__(WARPS * 32, 2) k_sweep2(S2Args a) {
     const uint64_t chunk = (a.ntiles + nwarps - 1) / nwarps;
     const uint64_t i0 = gw * chunk;
     const uint64_t i1 = min(i0 + chunk, a.ntiles);
+    const int ntile_w = wuni(i1 > i0 ? (int)(i1 - i0) : 0);
     const uint32_t fullm = (1u << a.N) - 1u;
     const uint32_t ulane = (uint32_t)lane;
+
+    Stream<MODE> st;
+    st.init(a.N);
+    const int total_blocks = ntile_w * st.nb;
+    int issued = 0, consumed = 0;
+    // issue blocks [issued, min(upto, total)) in batches: lane l issues block issued + l
+    auto produce = [&](int upto) {
+        upto = min(upto, total_blocks);
+        while (issued + G <= upto || (issued < upto && upto == total_blocks)) {
+            const int nbatch = min(G, upto - issued);
+            if (lane < nbatch) {
+                const int gb = issued + lane;
+                const int tt = gb / st.nb, b = gb - tt * st.nb;
+                const uint32_t tix = __ldg(a.order + i0 + tt);
+                const int slot = gb % RING;
+                tma_load_1k(ring + slot * 128, st.src(a, tix, b), &bars[slot]);
+            }
+            issued += nbatch;
+        }
+    };
+    // wait for the next block, copy it to registers, release the slot
+    auto consume4 = [&](double (&v)[4]) {
+        const int slot = consumed % RING;
+        mbar_wait(&bars[slot], (unsigned)((consumed / RING) & 1));
+        const double *blk = ring + slot * 128;
+#pragma unroll
+        for (int r = 0; r < 4; r++) v[r] = blk[r * 32 + lane];
+        __syncwarp();
+        consumed++;
+        produce(consumed + RING);
+    };
+    auto consume_ok = [&](double2 (&v)[4]) {   // two blocks of 64 double2: r = 0,1 then r = 2,3
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int slot = consumed % RING;
+            mbar_wait(&bars[slot], (unsigned)((consumed / RING) & 1));
+            const double2 *blk = reinterpret_cast<const double2 *>(ring + slot * 128);
+            v[2 * h] = blk[lane];
+            v[2 * h + 1] = blk[32 + lane];
+            __syncwarp();
+            consumed++;
+            produce(consumed + RING);
+        }
+    };
 
     double mu_lane = 0.0;
 #pragma unroll
@@ -351,84 +492,84 @@ __global__ void __launch_bounds__(WARPS * 32, 2) k_sweep2(S2Args a) {
 #pragma unroll
         for (int v = 0; v < NV; v++) bins[k][v] = 0.0;
     int curK = -1;
-    const double *__restrict__ Q = a.Q;
+    produce(RING);
+    if (ntile_w > 0) prefetch_prog(a, i0, lane);
 
-    for (uint64_t i = i0; i < i1; i++) {
-        const uint32_t t = __ldg(a.order + i);
+    for (int it = 0; it < ntile_w; it++) {
+        const uint64_t i = i0 + it;
+        const uint32_t t = (uint32_t)wuni((int)__ldg(a.order + i));
         const int K = __popc(t);
         const uint32_t jb = t << PROG_TB;
-        // issue the tile's global loads first: own-index neighbours, old p, scatter weights, program
-        double qo[4];
-#pragma unroll
-        for (int r = 0; r < 4; r++) qo[r] = __ldg(Q + jb + r * 32 + lane);
-        double pold[4];
-        if (MODE != 0) {
-#pragma unroll
-            for (int r = 0; r < 4; r++) pold[r] = a.P[jb + r * 32 + lane];
-        }
-        const uint32_t o = __ldg(a.off16 + i);
-        const uint32_t nrec = ((i + 1 < a.ntiles) ? __ldg(a.off16 + i + 1) : a.total16) - o;
-        __syncwarp();
-        for (uint32_t k = lane; k < nrec; k += 32) my[k] = __ldg(a.prog + o + k);
+        if (it + 1 < ntile_w) prefetch_prog(a, i + 1, lane);
         if (K != curK) {
             flush_bins<NV>(bins, curK, a.c, pcl, lane, wacc[warp]);
             curK = K;
         }
-        __syncwarp();
+        double qo[4];
+        consume4(qo);
+        double pold[4];
+        if (MODE >= 1) consume4(pold);
+        const uint4 *__restrict__ my = a.prog + __ldg(a.off16 + i);
+        const uint32_t *__restrict__ mycnt = reinterpret_cast<const uint32_t *>(my);
+        const double *__restrict__ myw0 = reinterpret_cast<const double *>(my + PROG_CNT16);
         const int beta = (a.c ^ K ^ pcl) & 1;
         int pp = PROG_HDR16;
         double A[4] = {0.0, 0.0, 0.0, 0.0}, D[4] = {0.0, 0.0, 0.0, 0.0};
         double mu_fix = 0.0;
-        // ---- varying units 0..7 (per-state busy status)
-        {   // unit 0: the implied parity bit; busy in state r iff beta ^ parity(r)
+        // ---- unit 0 (implied parity bit): busy in r iff b0(r) = beta ^ parity(r)
+        {
+            const uint32_t cw = (uint32_t)wuni((int)__ldg(mycnt + 0));
+            const double Wt = lane_pairs(my, pp, (int)(cw & 0xffffu), ulane, __ldg(myw0 + 0));
             const double nu = a.nu[0];
-            const uint32_t fr0 = (uint32_t)(beta ^ 1), fr1 = (uint32_t)beta;   // free in r with parity 0 / 1
-            pfma(D[0], nu, qo[0], fr0);
-            pfma(D[1], nu, qo[1], fr1);
-            pfma(D[2], nu, qo[2], fr1);
-            pfma(D[3], nu, qo[3], fr0);
-            apply_pairs(my, pp, mycnt[0], ulane, beta, qo, A);
+            const double We = beta ? Wt : 0.0, Wo = beta ? 0.0 : Wt;   // r = 0,3 / r = 1,2
+            const double ne = beta ? 0.0 : nu, no = beta ? nu : 0.0;
+            A[0] = fma(We, qo[0], A[0]);
+            A[3] = fma(We, qo[3], A[3]);
+            A[1] = fma(Wo, qo[1], A[1]);
+            A[2] = fma(Wo, qo[2], A[2]);
+            D[0] = fma(ne, qo[0], D[0]);
+            D[3] = fma(ne, qo[3], D[3]);
+            D[1] = fma(no, qo[1], D[1]);
+            D[2] = fma(no, qo[2], D[2]);
+            reg_pairs(my, pp, (int)(cw >> 16), ulane, beta, qo, A);
         }
+        // ---- lane units 1..5: busy per lane; own lane bit is part of every pattern
 #pragma unroll
         for (int u = 1; u <= 5; u++) {
             double q[4];
 #pragma unroll
             for (int r = 0; r < 4; r++) q[r] = __shfl_xor_sync(0xffffffffu, qo[r], 1 << (u - 1));
-            const double nu = a.nu[u];
-            const uint32_t fr = ((lane >> (u - 1)) & 1) ^ 1;
+            const uint32_t cw = (uint32_t)wuni((int)__ldg(mycnt + u));
+            const double Wt = lane_pairs(my, pp, (int)(cw & 0xffffu), ulane, 0.0);
+            const double nut = ((lane >> (u - 1)) & 1) ? 0.0 : a.nu[u];
 #pragma unroll
-            for (int r = 0; r < 4; r++) pfma(D[r], nu, q[r], fr);
-            apply_pairs(my, pp, mycnt[u], ulane, beta, q, A);
+            for (int r = 0; r < 4; r++) {
+                A[r] = fma(Wt, q[r], A[r]);
+                D[r] = fma(nut, q[r], D[r]);
+            }
+            reg_pairs(my, pp, (int)(cw >> 16), ulane, beta, q, A);
         }
+        // ---- register units 6, 7: busy in the register states with the bit set
 #pragma unroll
         for (int u = 6; u <= 7; u++) {
+            const int bit = 1 << (u - 6);
             double q[4];
 #pragma unroll
-            for (int r = 0; r < 4; r++) q[r] = qo[r ^ (1 << (u - 6))];
+            for (int r = 0; r < 4; r++) q[r] = qo[r ^ bit];
+            const uint32_t cw = (uint32_t)wuni((int)__ldg(mycnt + u));
+            const double Wt = lane_pairs(my, pp, (int)(cw & 0xffffu), ulane, __ldg(myw0 + u));
             const double nu = a.nu[u];
 #pragma unroll
-            for (int r = 0; r < 4; r++)
-                if (!((r >> (u - 6)) & 1)) D[r] = fma(nu, q[r], D[r]);
-            apply_pairs(my, pp, mycnt[u], ulane, beta, q, A);
-        }
-        // ---- fixed units 8..N-1 (tile-uniform busy status), one unit of prefetch
-        double qn[4];
-        {
-            const double *__restrict__ qp = Q + (jb ^ (1u << 7)) + lane;
-#pragma unroll
-            for (int r = 0; r < 4; r++) qn[r] = (a.N > 8) ? __ldg(qp + r * 32) : 0.0;
-        }
-#pragma unroll
-        for (int u = 8; u < HQ_MAXN; u++) {
-            if (u >= a.N) break;
-            double q[4];
-#pragma unroll
-            for (int r = 0; r < 4; r++) q[r] = qn[r];
-            if (u + 1 < a.N) {
-                const double *__restrict__ qp = Q + (jb ^ (1u << u)) + lane;
-#pragma unroll
-                for (int r = 0; r < 4; r++) qn[r] = __ldg(qp + r * 32);
+            for (int r = 0; r < 4; r++) {
+                if (r & bit) A[r] = fma(Wt, q[r], A[r]);
+                else D[r] = fma(nu, q[r], D[r]);
             }
+            reg_pairs(my, pp, (int)(cw >> 16), ulane, beta, q, A);
+        }
+        // ---- fixed units 8..N-1 (tile-uniform busy status), neighbour blocks from the ring
+        for (int u = PROG_NVARY; u < a.N; u++) {
+            double q[4];
+            consume4(q);
             const double nu = a.nu[u];
             if (!((t >> (u - PROG_NVARY)) & 1u)) {
 #pragma unroll
@@ -436,10 +577,11 @@ __global__ void __launch_bounds__(WARPS * 32, 2) k_sweep2(S2Args a) {
                 continue;
             }
             mu_fix += nu;
-            const double w0 = myw0[u];
+            const uint32_t cw = (uint32_t)wuni((int)__ldg(mycnt + u));
+            const double Wt = lane_pairs(my, pp, (int)(cw & 0xffffu), ulane, __ldg(myw0 + u));
 #pragma unroll
-            for (int r = 0; r < 4; r++) A[r] = fma(w0, q[r], A[r]);
-            apply_pairs(my, pp, mycnt[u], ulane, beta, q, A);
+            for (int r = 0; r < 4; r++) A[r] = fma(Wt, q[r], A[r]);
+            reg_pairs(my, pp, (int)(cw >> 16), ulane, beta, q, A);
         }
         // ---- lambda_m (blocked pseudo-unit for truncated lists)
         double lam[4];
@@ -448,14 +590,16 @@ __global__ void __launch_bounds__(WARPS * 32, 2) k_sweep2(S2Args a) {
             for (int r = 0; r < 4; r++) lam[r] = a.Lam;
         } else {
             const int u = a.N;
-            const double w0 = myw0[u];
-            double Bk[4] = {w0, w0, w0, w0};
+            const uint32_t cw = (uint32_t)wuni((int)__ldg(mycnt + u));
+            const double Bt = lane_pairs(my, pp, (int)(cw & 0xffffu), ulane, __ldg(myw0 + u));
+            double Bk[4] = {Bt, Bt, Bt, Bt};
             const double one[4] = {1.0, 1.0, 1.0, 1.0};
-            apply_pairs(my, pp, mycnt[u], ulane, beta, one, Bk);
+            reg_pairs(my, pp, (int)(cw >> 16), ulane, beta, one, Bk);
 #pragma unroll
             for (int r = 0; r < 4; r++) lam[r] = a.Lam - Bk[r];
         }
-        const double2 *__restrict__ okp = a.omkap;
+        double2 okv[4];
+        if (MODE < 2) consume_ok(okv);
 #pragma unroll
         for (int r = 0; r < 4; r++) {
             const int pr = __popc(r);
@@ -477,7 +621,7 @@ __global__ void __launch_bounds__(WARPS * 32, 2) k_sweep2(S2Args a) {
                 const double rden = __drcp_rn(den);
                 const double p = (s_x[n] * A[r] + s_y[n] * D[r]) * rden;
                 a.P[j] = p;
-                const double2 ok = __ldg(okp + j);
+                const double2 ok = okv[r];
                 bins[pr][0] += p;
                 bins[pr][1] += p * ok.x;
                 bins[pr][2] += p * ok.y;
@@ -488,7 +632,6 @@ __global__ void __launch_bounds__(WARPS * 32, 2) k_sweep2(S2Args a) {
     }
     flush_bins<NV>(bins, curK, a.c, pcl, lane, wacc[warp]);
     __syncthreads();
-    // map the kernel's value slots onto the reduction layout V2_*
     double *out = a.partial + (size_t)blockIdx.x * HQ_NL * HQ_NV;
     for (int i = tid; i < HQ_NL * HQ_NV; i += blockDim.x) {
         const int L = i / HQ_NV, v = i % HQ_NV;
@@ -647,7 +790,7 @@ cudaError_t prog_write(const P2Args &a, const uint32_t *order, const uint32_t *o
     hq2::k_prog_write<<<grid, 128, 0, s>>>(a, order, off16, prog);
     return cudaGetLastError();
 }
-size_t sweep_smem(uint32_t maxrec) { return sizeof(uint4) * (size_t)maxrec * hq2::WARPS; }
+size_t sweep_smem(uint32_t maxrec) { (void)maxrec; return sizeof(double) * 128 * hq2::RING * hq2::WARPS; }
 
 template <int MODE, int NV, bool FULL>
 static cudaError_t launch_sweep(const S2Args &a, int grid, cudaStream_t s) {

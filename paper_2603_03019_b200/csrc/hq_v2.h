@@ -9,14 +9,15 @@
 #define PROG_TB 7
 #define PROG_TILE 128
 #define PROG_NVARY 8
-// Program record (16-byte units): [0..3] per-unit pair counts (u16 x 32),
-// [4..19] W0[32] (fp64; zero for the varying units 0..7, whose contributions
-// are all pairs carrying the unit's own bit), then pairs
+// Program record (16-byte units): [0..7] per-unit pair counts (u32 x 32:
+// low 16 bits lane-only pairs, high 16 bits register-state pairs),
+// [8..23] W0[32] (fp64; zero for the lane units 1..5, whose contributions are
+// all pairs carrying the unit's own lane bit), then pairs
 // {c: fp64, w: u32 = lane5 | rm(beta=0) << 8 | rm(beta=1) << 12 | unit << 16, pad}
 // sorted by unit.  Unit index N is the "blocked" pseudo-unit (truncated
 // lists): sum of lambda_j over atoms whose whole list is busy.
-#define PROG_CNT16 4
-#define PROG_HDR16 20
+#define PROG_CNT16 8
+#define PROG_HDR16 24
 #define PROG_MAXPAIRS 1024
 
 // per-layer values reduced by the sweep kernel

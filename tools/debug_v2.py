@@ -69,17 +69,18 @@ prog = hq.hq_debug_copy(s.h, 3, 16 * total16, np.uint32).reshape(-1, 4)
 maxerr = 0.0
 for i in range(nt):
     t = int(order[i]); o = int(off[i])
-    cw = prog[o:o + 4].reshape(-1)
-    cnt = [(int(cw[u >> 1]) >> ((u & 1) * 16)) & 0xffff for u in range(32)]
-    w0 = prog[o + 4:o + 20].reshape(-1).view(np.float64)
-    pp = o + 20
+    cw = prog[o:o + 8].reshape(-1)
+    cnt = [(int(cw[u]) & 0xffff) + (int(cw[u]) >> 16) for u in range(32)]
+    cls = [(int(cw[u]) & 0xffff) for u in range(32)]
+    w0 = prog[o + 8:o + 24].reshape(-1).view(np.float64)
+    pp = o + 24
     pairs = {}
     for u in range(N + 1):
         pairs[u] = []
         for k in range(cnt[u]):
             rec = prog[pp + k]
             c = np.array([rec[0], rec[1]], dtype=np.uint32).view(np.float64)[0]
-            pairs[u].append((c, int(rec[2])))
+            pairs[u].append((c, int(rec[2]), k < cls[u]))
         pp += cnt[u]
     for cls in (0, 1):
         for r in range(4):
@@ -93,8 +94,12 @@ for i in range(nt):
                     if not (m >> u) & 1:
                         continue
                     w = w0[u]
-                    for c, wd in pairs[u]:
+                    for c, wd, laneonly in pairs[u]:
                         tl = ((wd & 31) & ~lane) == 0
+                        if laneonly:
+                            if tl:
+                                w += c
+                            continue
                         m4 = ((wd >> (8 + 4 * beta)) & 15) if tl else 0
                         if (m4 >> r) & 1:
                             w += c
