@@ -25,6 +25,7 @@
 #include "../../include/hq.h"
 #include "hq_internal.h"
 #include "hq_v2.h"
+#include "hq_v3.h"
 
 namespace hqk_launch {
 cudaError_t gather(const KArgs &k, int grid, cudaStream_t s);
@@ -209,6 +210,77 @@ std::vector<int> choose_perm(int N, const TrieHost &tr) {
     return perm;
 }
 
+
+// Internal unit order for the CTA-tiled path (hq_v3.h): units 0 (parity),
+// 1, 7, 8 (register bits), 2..6 (lanes), 9..8+nW (warps) vary inside a tile;
+// the rest ("H") are fixed per tile.  Units that most often precede other
+// units in the preference lists become H (their nodes fold into the
+// tile-uniform rate part); among the varying units, the four register-class
+// slots go to the units whose choice minimises the expected cost of
+// register-dependent pairs (about 8x a lane-only pair) over random tiles.
+std::vector<int> choose_perm_v3(int N, const TrieHost &tr, int nW) {
+    const int NVU = 9 + nW;
+    std::vector<int> perm(N);
+    for (int u = 0; u < N; u++) perm[u] = u;
+    const char *env = getenv("HQ_PERM");
+    if (env && std::string(env) == "identity") return perm;
+    std::vector<long> cnt(N, 0);
+    std::vector<int> stk;
+    std::vector<uint32_t> pre(tr.node.size()), pstk;
+    for (size_t v = 0; v < tr.node.size(); v++) {
+        const int u = tr.node[v].x & 0xff, d = (tr.node[v].x >> 8) & 0xff;
+        stk.resize(d - 1);
+        pstk.resize(d - 1);
+        for (int a : stk) cnt[a]++;
+        pre[v] = d >= 2 ? pstk[d - 2] : 0u;
+        stk.push_back(u);
+        pstk.push_back(pre[v] | (1u << u));
+    }
+    std::vector<int> idx(N);
+    for (int u = 0; u < N; u++) idx[u] = u;
+    std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return cnt[a] < cnt[b]; });
+    std::vector<int> V(idx.begin(), idx.begin() + NVU);
+    uint32_t vmask = 0;
+    for (int x : V) vmask |= 1u << x;
+    // node weight: probability that its tile-unit prefix is busy in a random tile
+    std::vector<double> w(tr.node.size());
+    for (size_t v = 0; v < tr.node.size(); v++) {
+        const int u = tr.node[v].x & 0xff;
+        const uint32_t path = pre[v] | (1u << u);
+        w[v] = std::ldexp(1.0, -__builtin_popcount(path & ~vmask));
+    }
+    double best = 1e300;
+    uint32_t bestT = 0;
+    const int nv = (int)V.size();
+    for (int a1 = 0; a1 < nv; a1++)
+        for (int a2 = a1 + 1; a2 < nv; a2++)
+            for (int a3 = a2 + 1; a3 < nv; a3++)
+                for (int a4 = a3 + 1; a4 < nv; a4++) {
+                    const uint32_t T = (1u << V[a1]) | (1u << V[a2]) | (1u << V[a3]) | (1u << V[a4]);
+                    double cost = 0.0;
+                    for (size_t v = 0; v < tr.node.size(); v++) {
+                        const uint32_t S = pre[v] & vmask;
+                        if (!S) continue;
+                        cost += (S & T) ? 8.0 * w[v] : w[v];
+                    }
+                    if (cost < best) {
+                        best = cost;
+                        bestT = T;
+                    }
+                }
+    std::vector<int> regc, rest;
+    for (int x : V) ((bestT >> x) & 1u ? regc : rest).push_back(x);
+    perm[0] = regc[0];
+    perm[1] = regc[1];
+    perm[7] = regc[2];
+    perm[8] = regc[3];
+    int k = 0;
+    for (int u = 2; u <= 6; u++) perm[u] = rest[k++];
+    for (int u = 9; u < NVU; u++) perm[u] = rest[k++];
+    for (int q = NVU; q < N; q++) perm[q] = idx[q];
+    return perm;
+}
+
 }  // namespace
 
 struct hq_problem {
@@ -239,6 +311,8 @@ struct hq_problem {
     int grid = 0;
     // v2 (N >= 8) device state
     bool v2 = false, v2_ready = false;
+    int path = 1;                  // 1: N < 8 two-pass, 2: warp-tiled (hq_v2.cu), 3: CTA-tiled (hq_v3.cu)
+    int nW = 0;                    // path 3: log2(warps per CTA)
     uint32_t *d_order = nullptr, *d_off16 = nullptr, *d_size16 = nullptr;
     uint4 *d_prog = nullptr;
     double2 *d_omkap = nullptr;
@@ -367,7 +441,14 @@ extern "C" hq_status hq_create(int N, int J, const double *lambda, const double 
     h->pref.assign(pref, pref + (size_t)J * N);
     {
         TrieHost abi = build_trie(N, J, lambda, pref);
-        h->perm = choose_perm(N, abi);
+        const char *penv = getenv("HQ_PATH");
+        h->path = N < 8 ? 1 : (N < 9 || (penv && std::string(penv) == "2")) ? 2 : 3;
+        if (h->path == 3) {
+            h->nW = hq3_launch::choose_nw(N);
+            h->perm = choose_perm_v3(N, abi, h->nW);
+        } else {
+            h->perm = choose_perm(N, abi);
+        }
         std::vector<int> inv(N);
         for (int u = 0; u < N; u++) inv[h->perm[u]] = u;
         std::vector<int32_t> pint((size_t)J * N);
@@ -398,7 +479,12 @@ static hq_status ensure_device(hq_problem *h) {
     h->grid = (int)std::min<uint64_t>(ntiles, (uint64_t)h->nsm * 4);
     const size_t nn = h->trie.node.size();
     auto alloc = [&](void **p, size_t bytes) -> cudaError_t { return cudaMalloc(p, bytes ? bytes : 16); };
-    h->sgrid = hq2_launch::sweep_grid(h->nsm);
+    if (h->path == 3) {
+        const uint64_t nt3 = 1ull << (N - 9 - h->nW);
+        h->sgrid = (int)std::min<uint64_t>(nt3, (uint64_t)h->nsm * std::max(1, 16 >> h->nW));
+    } else {
+        h->sgrid = hq2_launch::sweep_grid(h->nsm);
+    }
     if (alloc((void **)&h->d_pw, sizeof(double) * S) != cudaSuccess ||
         (!h->v2 && alloc((void **)&h->d_ab, sizeof(double2) * (S >> 1 ? S >> 1 : 1)) != cudaSuccess) ||
         (h->v2 && alloc((void **)&h->d_omkap, sizeof(double2) * S) != cudaSuccess)) {
@@ -504,7 +590,7 @@ static hq_status v2_prepare(hq_problem *h, cudaStream_t s) {
     if (h->v2_ready) return HQ_OK;
     const int N = h->N;
     const uint64_t S = 1ull << N, half = S >> 1;
-    const int Nt = N - 8;
+    const int Nt = h->path == 3 ? N - 9 - h->nW : N - 8;
     const uint64_t ntiles = 1ull << Nt;
     // tile visit order: by popcount of the tile index, ascending within a popcount class
     std::vector<uint32_t> order;
@@ -547,7 +633,18 @@ static hq_status v2_prepare(hq_problem *h, cudaStream_t s) {
     if (!h->full_lists) HQ_CUDA(hq2_launch::lambda_states(pa, h->d_lamarr, g, s));
     HQ_CUDA(hq2_launch::omkap(pa, h->d_lamarr, h->d_omkap, g, s));
     HQ_CUDA(cudaMemsetAsync(h->d_err, 0, sizeof(int), s));
-    HQ_CUDA(hq2_launch::prog_count(pa, h->d_order, h->d_size16, h->d_err, g, s));
+    P3Args p3;
+    memset(&p3, 0, sizeof(p3));
+    p3.N = N;
+    p3.nW = h->nW;
+    p3.full_lists = pa.full_lists;
+    p3.ntiles = ntiles;
+    p3.nnodes = pa.nnodes;
+    p3.node = pa.node;
+    p3.lam_thr = pa.lam_thr;
+    p3.lam_end = pa.lam_end;
+    if (h->path == 3) HQ_CUDA(hq3_launch::prog_count(p3, h->d_order, h->d_size16, h->d_err, g, s));
+    else HQ_CUDA(hq2_launch::prog_count(pa, h->d_order, h->d_size16, h->d_err, g, s));
     size_t tmpb = 0;
     HQ_CUDA(hq2_launch::prog_scan(h->d_size16, h->d_off16, ntiles, nullptr, &tmpb, s));
     void *tmp = nullptr;
@@ -570,7 +667,8 @@ static hq_status v2_prepare(hq_problem *h, cudaStream_t s) {
     cudaFree(tmp);
     cudaFree(tmp2);
     cudaFree(d_max);
-    if (hq2_launch::sweep_smem(h->maxrec) > 150 * 1024) {
+    const size_t smem_need = h->path == 3 ? hq3_launch::sweep_smem(h->nW, h->maxrec) : hq2_launch::sweep_smem(h->maxrec);
+    if (smem_need > (h->path == 3 ? 220u * 1024u : 150u * 1024u)) {
         h->err = "rate program of a tile exceeds the shared-memory budget";
         return HQ_E_NUMERIC;
     }
@@ -585,7 +683,8 @@ static hq_status v2_prepare(hq_problem *h, cudaStream_t s) {
         h->err = "device memory for the rate programs could not be allocated";
         return HQ_E_NOMEM;
     }
-    HQ_CUDA(hq2_launch::prog_write(pa, h->d_order, h->d_off16, h->d_prog, g, s));
+    if (h->path == 3) HQ_CUDA(hq3_launch::prog_write(p3, h->d_order, h->d_off16, h->d_prog, g, s));
+    else HQ_CUDA(hq2_launch::prog_write(pa, h->d_order, h->d_off16, h->d_prog, g, s));
     HQ_CUDA(cudaEventRecord(e1, s));
     HQ_CUDA(cudaEventSynchronize(e1));
     float ms = 0.f;
@@ -597,6 +696,32 @@ static hq_status v2_prepare(hq_problem *h, cudaStream_t s) {
     (void)half;
     h->v2_ready = true;
     return HQ_OK;
+}
+
+// one sweep / residual launch of the tiled paths (2: hq_v2.cu, 3: hq_v3.cu)
+static cudaError_t tiled_sweep(hq_problem *h, const S2Args &sa, int mode, cudaStream_t s) {
+    if (h->path != 3) return hq2_launch::sweep(sa, mode, h->sgrid, s);
+    S3Args a;
+    memset(&a, 0, sizeof(a));
+    a.N = sa.N;
+    a.nW = h->nW;
+    a.c = sa.c;
+    a.active = sa.active;
+    a.ntiles = sa.ntiles;
+    a.chunk = (sa.ntiles + h->sgrid - 1) / h->sgrid;
+    a.Lam = sa.Lam;
+    for (int u = 0; u < 32; u++) a.nu[u] = sa.nu[u];
+    a.order = sa.order;
+    a.off16 = sa.off16;
+    a.prog = sa.prog;
+    a.total16 = sa.total16;
+    a.maxrec16 = sa.maxrec;
+    a.Q = sa.Q;
+    a.P = sa.P;
+    a.omkap = sa.omkap;
+    a.coef = sa.coef;
+    a.partial = sa.partial;
+    return hq3_launch::sweep(a, sa.full_lists, mode, h->sgrid, s);
 }
 
 struct SolveOut {
@@ -615,7 +740,7 @@ static hq_status v2_residual(hq_problem *h, cudaStream_t s, S2Args sa, SolveOut 
         sa.P = h->d_pw + (c ? half : 0);
         sa.Q = h->d_pw + (c ? 0 : half);
         sa.partial = h->d_partial + (size_t)c * h->sgrid * HQ_NL * HQ_NV;
-        HQ_CUDA(hq2_launch::sweep(sa, 2, h->sgrid, s));
+        HQ_CUDA(tiled_sweep(h, sa, 2, s));
     }
     HQ_CUDA(cudaEventRecord(eb, s));
     HQ_CUDA(hq2_launch::scalars(N, sa.full_lists, h->Lam, 2, 0, 0, 2 * h->sgrid, h->d_partial, h->d_blk, s));
@@ -660,7 +785,7 @@ static hq_status solve_v2(hq_problem *h, double tol, int max_iter, double *pi, c
     memset(&sa, 0, sizeof(sa));
     sa.N = N;
     sa.full_lists = h->full_lists ? 1 : 0;
-    sa.ntiles = 1ull << (N - 8);
+    sa.ntiles = 1ull << (h->path == 3 ? N - 9 - h->nW : N - 8);
     sa.Lam = h->Lam;
     for (int u = 0; u < 32; u++) sa.nu[u] = u < N ? h->nu_int[u] : 0.0;
     sa.order = h->d_order;
@@ -689,7 +814,7 @@ static hq_status solve_v2(hq_problem *h, double tol, int max_iter, double *pi, c
         sa.partial = h->d_partial;
         const bool checking = tol > 0.0 && t >= next_check - 1;
         HQ_CUDA(cudaEventRecord(h->event(2 * (size_t)o.halfsweeps), s));
-        HQ_CUDA(hq2_launch::sweep(sa, checking ? 1 : 0, h->sgrid, s));
+        HQ_CUDA(tiled_sweep(h, sa, checking ? 1 : 0, s));
         HQ_CUDA(cudaEventRecord(h->event(2 * (size_t)o.halfsweeps + 1), s));
         HQ_CUDA(hq2_launch::scalars(N, sa.full_lists, h->Lam, 1, c, active, h->sgrid, h->d_partial, h->d_blk, s));
         o.launches += 2;
@@ -800,7 +925,7 @@ extern "C" hq_status hq_solve(hq_handle h, double tol, int max_iter, double *pi,
         h->stats[10] = o.resid_ms;
         h->stats[11] = h->precompute_ms;
         h->stats[12] = h->prog_bytes;
-        h->stats[13] = 2;   // path id
+        h->stats[13] = h->path;   // path id
         if (iters_out) *iters_out = o.sweeps;
         if (residual_out) *residual_out = o.res;
         if (!std::isfinite(o.res)) {

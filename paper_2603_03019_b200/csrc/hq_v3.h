@@ -1,0 +1,70 @@
+// hq_v3.h -- argument blocks and program format of the CTA-tiled sweep path
+// (hq_v3.cu).  Product code only; nothing here is shared with oracle/.
+//
+// Tile geometry (compressed index j of a parity class):
+//   bit 0            register bit 0   (internal unit 1)
+//   bits 1..5        lane bits        (internal units 2..6)
+//   bits 6..7        register bits 1-2 (internal units 7, 8)
+//   bits 8..8+nW-1   warp bits        (internal units 9 .. 8+nW)
+//   bits T.. (T=8+nW) tile index t    (internal units 9+nW .. N-1, "H" units)
+// Internal unit 0 is the implied parity unit: b0 = c ^ parity(j).
+// A CTA of 32 << nW threads owns one tile (2^T compressed states) at a time;
+// thread (warp w, lane l) owns the 8 states r = 0..7 of its (w, l) slot.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "hq_internal.h"
+
+#define V3_R 8                 // states per thread
+#define V3_RING 4              // per-warp ring slots (2 KB each)
+#define V3_SLOT 256            // doubles per ring slot (one warp's 256 states)
+#define V3_HDR16 24            // program header: info[32] (u32) + W0[32] (f64) = 24 x 16 B
+#define V3_MAXPAIRS 4096
+
+// program record (16-byte units):
+//   [0..7]   info[u] = n_lane | n_reg << 8 | start << 16   (u = 0..N; N = blocked pseudo-unit)
+//   [8..23]  W0[u] (f64)
+//   pairs    uint4 {c.lo, c.hi, S_t, rm}: S_t = thread-level condition (unit bits of the
+//            lane/warp units that must be busy), rm = admissible register states for
+//            beta = 0 (bits 0..7) and beta = 1 (bits 8..15); lane-only pairs first.
+
+struct S3Args {
+    int N;
+    int nW;                  // log2(warps per CTA)
+    int c;                   // class updated (sweep) / evaluated (residual)
+    uint32_t active;         // layers updated in this half-sweep
+    uint64_t ntiles;
+    uint64_t chunk;          // tiles per CTA (contiguous range of the visit order)
+    double Lam;
+    double nu[32];           // internal-order service rates
+    const uint32_t *order;   // tile visit order
+    const uint32_t *off16;   // program offset of visit index i (16-byte units)
+    const uint4 *prog;
+    uint32_t total16;
+    uint32_t maxrec16;       // largest program (16-byte units)
+    const double *Q;         // neighbour class (read)
+    double *P;               // updated class (sweep) / evaluated class (residual)
+    const double2 *omkap;    // scatter weights of class c
+    const double *coef;      // v2 scalar block (V2S_* offsets)
+    double *partial;         // [grid][HQ_NL][HQ_NV]
+};
+
+struct P3Args {   // program precompute
+    int N;
+    int nW;
+    int full_lists;
+    uint64_t ntiles;
+    int nnodes;
+    const int2 *node;        // .x = unit | depth << 8, .y = skip
+    const double *lam_thr;
+    const double *lam_end;
+};
+
+namespace hq3_launch {
+cudaError_t prog_count(const P3Args &a, const uint32_t *order, uint32_t *size16, int *err, int grid, cudaStream_t s);
+cudaError_t prog_write(const P3Args &a, const uint32_t *order, const uint32_t *off16, uint4 *prog, int grid,
+                       cudaStream_t s);
+cudaError_t sweep(const S3Args &a, int full, int mode, int grid, cudaStream_t s);
+size_t sweep_smem(int nW, uint32_t maxrec16);
+int choose_nw(int N);
+}  // namespace hq3_launch
