@@ -29,7 +29,8 @@ def _stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if force or _stale():
         nvcc = os.environ.get("NVCC", "nvcc")
-        cmd = [nvcc] + NVCC_FLAGS + (["-Xptxas", "-v"] if verbose else []) + ["-o", LIB] + SOURCES
+        extra = ["-DHQ_DEBUG_HANG"] if os.environ.get("HQ_DEBUG_HANG") else []
+        cmd = [nvcc] + NVCC_FLAGS + extra + (["-Xptxas", "-v"] if verbose else []) + ["-o", LIB] + SOURCES
         subprocess.run(cmd, check=True)
     return LIB
 

@@ -313,6 +313,7 @@ struct hq_problem {
     bool v2 = false, v2_ready = false;
     int path = 1;                  // 1: N < 8 two-pass, 2: warp-tiled (hq_v2.cu), 3: CTA-tiled (hq_v3.cu)
     int nW = 0;                    // path 3: log2(warps per CTA)
+    int nslots = 0;                // path 3: CTA ring slots
     uint32_t *d_order = nullptr, *d_off16 = nullptr, *d_size16 = nullptr;
     uint4 *d_prog = nullptr;
     double2 *d_omkap = nullptr;
@@ -607,15 +608,24 @@ static hq_status v2_prepare(hq_problem *h, cudaStream_t s) {
             x = (((r ^ x) >> 2) / cc) | r;
         }
     }
+    // path 3: rate programs are per warp tile, (t << nW) | w, stored tile by tile
+    const int nWp = h->path == 3 ? h->nW : 0;
+    const uint64_t nprog = ntiles << nWp;
+    if (nWp) {
+        std::vector<uint32_t> w(nprog);
+        for (uint64_t i = 0; i < ntiles; i++)
+            for (uint32_t x = 0; x < (1u << nWp); x++) w[(i << nWp) | x] = (order[i] << nWp) | x;
+        order.swap(w);
+    }
     auto alloc = [&](void **p, size_t bytes) -> cudaError_t { return cudaMalloc(p, bytes ? bytes : 16); };
-    if (alloc((void **)&h->d_order, 4 * ntiles) != cudaSuccess || alloc((void **)&h->d_off16, 4 * ntiles) != cudaSuccess ||
-        alloc((void **)&h->d_size16, 4 * ntiles) != cudaSuccess ||
+    if (alloc((void **)&h->d_order, 4 * nprog) != cudaSuccess || alloc((void **)&h->d_off16, 4 * nprog) != cudaSuccess ||
+        alloc((void **)&h->d_size16, 4 * nprog) != cudaSuccess ||
         (!h->full_lists && alloc((void **)&h->d_lamarr, 8 * S) != cudaSuccess)) {
         cudaGetLastError();
         h->err = "device memory for the tile tables could not be allocated";
         return HQ_E_NOMEM;
     }
-    HQ_CUDA(cudaMemcpyAsync(h->d_order, order.data(), 4 * ntiles, cudaMemcpyHostToDevice, s));
+    HQ_CUDA(cudaMemcpyAsync(h->d_order, order.data(), 4 * nprog, cudaMemcpyHostToDevice, s));
     P2Args pa;
     memset(&pa, 0, sizeof(pa));
     pa.N = N;
@@ -636,9 +646,9 @@ static hq_status v2_prepare(hq_problem *h, cudaStream_t s) {
     P3Args p3;
     memset(&p3, 0, sizeof(p3));
     p3.N = N;
-    p3.nW = h->nW;
     p3.full_lists = pa.full_lists;
-    p3.ntiles = ntiles;
+    p3.ntiles = nprog;
+    for (int u = 0; u < 32; u++) p3.nu[u] = pa.nu[u];
     p3.nnodes = pa.nnodes;
     p3.node = pa.node;
     p3.lam_thr = pa.lam_thr;
@@ -646,29 +656,43 @@ static hq_status v2_prepare(hq_problem *h, cudaStream_t s) {
     if (h->path == 3) HQ_CUDA(hq3_launch::prog_count(p3, h->d_order, h->d_size16, h->d_err, g, s));
     else HQ_CUDA(hq2_launch::prog_count(pa, h->d_order, h->d_size16, h->d_err, g, s));
     size_t tmpb = 0;
-    HQ_CUDA(hq2_launch::prog_scan(h->d_size16, h->d_off16, ntiles, nullptr, &tmpb, s));
+    HQ_CUDA(hq2_launch::prog_scan(h->d_size16, h->d_off16, nprog, nullptr, &tmpb, s));
     void *tmp = nullptr;
     HQ_CUDA(alloc(&tmp, tmpb));
-    HQ_CUDA(hq2_launch::prog_scan(h->d_size16, h->d_off16, ntiles, tmp, &tmpb, s));
+    HQ_CUDA(hq2_launch::prog_scan(h->d_size16, h->d_off16, nprog, tmp, &tmpb, s));
     uint32_t *d_max = nullptr;
     HQ_CUDA(alloc((void **)&d_max, 4));
     size_t tmpb2 = 0;
-    HQ_CUDA(hq2_launch::prog_max(h->d_size16, d_max, ntiles, nullptr, &tmpb2, s));
+    HQ_CUDA(hq2_launch::prog_max(h->d_size16, d_max, nprog, nullptr, &tmpb2, s));
     void *tmp2 = nullptr;
     HQ_CUDA(alloc(&tmp2, tmpb2));
-    HQ_CUDA(hq2_launch::prog_max(h->d_size16, d_max, ntiles, tmp2, &tmpb2, s));
+    HQ_CUDA(hq2_launch::prog_max(h->d_size16, d_max, nprog, tmp2, &tmpb2, s));
     uint32_t last[2] = {0, 0};
     int herr = 0;
     HQ_CUDA(cudaMemcpyAsync(&h->maxrec, d_max, 4, cudaMemcpyDeviceToHost, s));
-    HQ_CUDA(cudaMemcpyAsync(&last[0], h->d_off16 + ntiles - 1, 4, cudaMemcpyDeviceToHost, s));
-    HQ_CUDA(cudaMemcpyAsync(&last[1], h->d_size16 + ntiles - 1, 4, cudaMemcpyDeviceToHost, s));
+    HQ_CUDA(cudaMemcpyAsync(&last[0], h->d_off16 + nprog - 1, 4, cudaMemcpyDeviceToHost, s));
+    HQ_CUDA(cudaMemcpyAsync(&last[1], h->d_size16 + nprog - 1, 4, cudaMemcpyDeviceToHost, s));
     HQ_CUDA(cudaMemcpyAsync(&herr, h->d_err, sizeof(int), cudaMemcpyDeviceToHost, s));
     HQ_CUDA(cudaStreamSynchronize(s));
+    if (nWp) {   // largest program block of a CTA tile
+        std::vector<uint32_t> sz(nprog);
+        HQ_CUDA(cudaMemcpy(sz.data(), h->d_size16, 4 * nprog, cudaMemcpyDeviceToHost));
+        uint32_t mb = 0;
+        for (uint64_t i = 0; i < ntiles; i++) {
+            uint32_t b = 0;
+            for (uint32_t x = 0; x < (1u << nWp); x++) b += sz[(i << nWp) | x];
+            mb = std::max(mb, b);
+        }
+        h->maxrec = mb;
+    }
     cudaFree(tmp);
     cudaFree(tmp2);
     cudaFree(d_max);
-    const size_t smem_need = h->path == 3 ? hq3_launch::sweep_smem(h->nW, h->maxrec) : hq2_launch::sweep_smem(h->maxrec);
-    if (smem_need > (h->path == 3 ? 220u * 1024u : 150u * 1024u)) {
+    if (h->path == 3) {   // staged program capacity: <= 16 KB per buffer; larger blocks stay in global memory
+        h->maxrec = std::min<uint32_t>(h->maxrec, 2048u);
+        h->nslots = hq3_launch::choose_slots(h->nW, h->maxrec);
+    }
+    if (h->path == 3 ? h->nslots < 1 : hq2_launch::sweep_smem(h->maxrec) > 150u * 1024u) {
         h->err = "rate program of a tile exceeds the shared-memory budget";
         return HQ_E_NUMERIC;
     }
@@ -683,7 +707,15 @@ static hq_status v2_prepare(hq_problem *h, cudaStream_t s) {
         h->err = "device memory for the rate programs could not be allocated";
         return HQ_E_NOMEM;
     }
-    if (h->path == 3) HQ_CUDA(hq3_launch::prog_write(p3, h->d_order, h->d_off16, h->d_prog, g, s));
+    if (h->path == 3) {
+        HQ_CUDA(hq3_launch::prog_write(p3, h->d_order, h->d_off16, h->d_prog, h->d_err, g, s));
+        HQ_CUDA(cudaMemcpyAsync(&herr, h->d_err, sizeof(int), cudaMemcpyDeviceToHost, s));
+        HQ_CUDA(cudaStreamSynchronize(s));
+        if (herr) {
+            h->err = "rate program overflow (more than 255 lane-only pairs or groups for a unit)";
+            return HQ_E_NUMERIC;
+        }
+    }
     else HQ_CUDA(hq2_launch::prog_write(pa, h->d_order, h->d_off16, h->d_prog, g, s));
     HQ_CUDA(cudaEventRecord(e1, s));
     HQ_CUDA(cudaEventSynchronize(e1));
@@ -708,14 +740,15 @@ static cudaError_t tiled_sweep(hq_problem *h, const S2Args &sa, int mode, cudaSt
     a.c = sa.c;
     a.active = sa.active;
     a.ntiles = sa.ntiles;
-    a.chunk = (sa.ntiles + h->sgrid - 1) / h->sgrid;
+    a.chunk = 0;
     a.Lam = sa.Lam;
     for (int u = 0; u < 32; u++) a.nu[u] = sa.nu[u];
     a.order = sa.order;
     a.off16 = sa.off16;
     a.prog = sa.prog;
     a.total16 = sa.total16;
-    a.maxrec16 = sa.maxrec;
+    a.maxblk16 = sa.maxrec;
+    a.nslots = h->nslots;
     a.Q = sa.Q;
     a.P = sa.P;
     a.omkap = sa.omkap;

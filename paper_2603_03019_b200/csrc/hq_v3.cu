@@ -9,20 +9,24 @@
 // lambda(n)/mu(n+1) prepared a priori (hq_v2.cu k_scalars2, R1).
 //
 // Work decomposition (hq_v3.h): a CTA of 32 << nW threads owns one tile of
-// 2^T compressed states (T = 8 + nW) at a time.  Thread (w, l) owns 8 states.
+// 2^T compressed states (T = 8 + nW) at a time; thread (w, l) owns 8 states.
 // Neighbours across
 //   * register bits (units 1, 7, 8) come from the thread's own registers,
 //   * the implied parity unit 0 is the state's own index in the other class,
-//   * lane and warp bits (units 2..6, 9..8+nW) come from the tile's block of q
-//     staged in shared memory by one bulk copy (TMA engine, cp.async.bulk),
-//   * tile bits ("H" units) come from the neighbour tile's block, streamed per
-//     warp through a 4-slot ring of 2 KB bulk copies completed on mbarriers.
-// The upward rates are evaluated from a per-tile "rate program"
-// (Algorithm 3, evaluated symbolically for the 2^T states
-// of the tile): per unit a tile-uniform part W0_u plus pairs (c, S) added when
-// the varying units S are busy.  Pairs that depend only on lane/warp units
-// are summed once per thread; pairs that involve register units or the
-// parity unit carry an 8-bit mask of the admissible register states.
+//   * lane and warp bits (units 2..6, 9..8+nW) come from the tile's block of q,
+//     staged in shared memory (double-buffered across tiles) by bulk copies
+//     (cp.async.bulk, the TMA engine) completed on an mbarrier,
+//   * tile bits ("H" units) come from the neighbour tiles' blocks, streamed
+//     through a CTA-wide ring of tile-sized slots: the last warp to release a
+//     slot refills it with the block needed nslots items later.
+// The same ring streams the own old p (convergence proxy / residual) and the
+// scatter weights (omega, kappa) of the tile.
+//
+// Upward rates come from a per-tile "rate program" (Algorithm 3,
+// PAPER.md:541-567, evaluated symbolically for the 2^T states of the tile):
+// per unit a tile-uniform part W0_u, lane-only pairs (c, S_t) added when the
+// thread's lane/warp units S_t are busy, and groups of register-dependent
+// pairs sharing one mask of admissible register states.
 //
 // Per-layer sums (sum p, sum p omega, sum p kappa [, sum p lambda_m]
 // [, sum |dp|]) are accumulated in fixed order: per-thread bins, warp
@@ -30,6 +34,7 @@
 // over the warps of the CTA, and k_scalars2's fixed-order sum over CTAs.
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <cstdio>
 #include "hq_internal.h"
 #include "hq_v2.h"
 #include "hq_v3.h"
@@ -37,7 +42,6 @@
 namespace hq3 {
 
 constexpr int R = V3_R;
-constexpr int RING = V3_RING;
 
 __device__ __forceinline__ double warp_sum(double s) {
 #pragma unroll
@@ -46,30 +50,51 @@ __device__ __forceinline__ double warp_sum(double s) {
 }
 __device__ __forceinline__ int wuni(int x) { return (int)__reduce_max_sync(0xffffffffu, (unsigned)x); }
 
-__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
-    asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count));
+__device__ __forceinline__ unsigned sptr(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
+    asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(bar), "r"(count));
 }
-__device__ __forceinline__ void mbar_expect(uint64_t *bar, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)),
-                 "r"(bytes)
+__device__ __forceinline__ void mbar_expect(unsigned bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(unsigned dst, const void *src, unsigned bytes, unsigned bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
                  : "memory");
 }
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     (unsigned)__cvta_generic_to_shared(dst)),
-                 "l"(src), "r"(bytes), "r"((unsigned)__cvta_generic_to_shared(bar))
-                 : "memory");
+#ifdef HQ_DEBUG_HANG
+// bounded wait: reports the barrier and traps instead of hanging (debug builds)
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+    for (long it = 0;; it++) {
+        unsigned ok;
+        asm volatile(
+            "{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared.b64 P1, [%1], %2;\n\tselp.u32 %0, 1, 0, P1;\n\t}"
+            : "=r"(ok)
+            : "r"(bar), "r"(parity)
+            : "memory");
+        if (ok) return;
+        if (it == 20000000) {
+            printf("hq3 hang: block %d thread %d bar 0x%x parity %u\n", blockIdx.x, threadIdx.x, bar, parity);
+            __trap();
+        }
+    }
 }
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
-    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+#else
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
     asm volatile(
         "{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
         "mbarrier.try_wait.parity.shared.b64 P1, [%0], %1;\n\t"
-        "@!P1 bra WAIT_%=;\n\t}" ::"r"(b),
+        "@!P1 bra WAIT_%=;\n\t}" ::"r"(bar),
         "r"(parity)
         : "memory");
 }
+#endif
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ unsigned atom_add_acqrel(unsigned addr, unsigned v) {
+    unsigned old;
+    asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(addr), "r"(v) : "memory");
+    return old;
+}
 
 // acc += a * b if pred != 0 (forced predication)
 __device__ __forceinline__ void pfma(double &acc, double a, double b, uint32_t pred) {
@@ -77,28 +102,65 @@ __device__ __forceinline__ void pfma(double &acc, double a, double b, uint32_t p
         : "+d"(acc)
         : "d"(a), "d"(b), "r"(pred));
 }
-
-__device__ __forceinline__ double rec_c(const uint4 &x) { return __hiloint2double((int)x.y, (int)x.x); }
-
-// tile-uniform part plus the lane-only pairs whose thread-level condition holds
-__device__ __forceinline__ double lane_pairs(const uint4 *__restrict__ rec, int n, uint32_t busy_t, double W) {
-    for (int k = 0; k < n; k++) {
-        const uint4 x = rec[k];
-        if ((x.z & ~busy_t) == 0u) W += rec_c(x);
-    }
-    return W;
+// W += c if (S & nb) == 0, nb = ~busy (forced predication)
+__device__ __forceinline__ void padd(double &W, const uint4 &x, uint32_t nb) {
+    asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\t.reg .f64 c;\n\t"
+        "and.b32 t, %3, %4;\n\tsetp.eq.u32 p, t, 0;\n\tmov.b64 c, {%1, %2};\n\t@p add.f64 %0, %0, c;\n\t}"
+        : "+d"(W)
+        : "r"(x.x), "r"(x.y), "r"(x.z), "r"(nb));
 }
 
-// register-dependent pairs: A[r] += c q[r] for the admissible states r
-__device__ __forceinline__ void reg_pairs(const uint4 *__restrict__ rec, int n, uint32_t busy_t, int sh,
-                                          const double (&q)[R], double (&A)[R]) {
-    for (int k = 0; k < n; k++) {
-        const uint4 x = rec[k];
-        const double c = rec_c(x);
-        const uint32_t m8 = ((x.z & ~busy_t) == 0u) ? ((x.w >> sh) & 0xffu) : 0u;
-#pragma unroll
-        for (int r = 0; r < R; r++) pfma(A[r], c, q[r], m8 & (1u << r));
+// tile-uniform part plus the lane-only pairs whose thread-level condition holds
+// (two interleaved partial sums for ILP; fixed order)
+__device__ __forceinline__ double lane_pairs(const uint4 *__restrict__ rec, int n, uint32_t nb, double W) {
+    double W2 = 0.0;
+    int k = 0;
+    for (; k + 1 < n; k += 2) {
+        const uint4 x = rec[k], y = rec[k + 1];
+        padd(W, x, nb);
+        padd(W2, y, nb);
     }
+    if (k < n) padd(W, rec[k], nb);
+    return W + W2;
+}
+
+// register-dependent groups: A[r] += w_g q[r] for the admissible states r of group g
+__device__ __forceinline__ void reg_groups(const uint4 *__restrict__ rec, int ng, uint32_t nb, int sh,
+                                           const double (&q)[R], double (&A)[R]) {
+    for (int g = 0; g < ng; g++) {
+        const uint4 hd = rec[0];
+        const int n = (int)hd.z;
+#ifdef HQ_DEBUG_HANG
+        if (n > V3_MAXPAIRS) {
+            printf("hq3 corrupt group: block %d thread %d n %d g %d/%d\n", blockIdx.x, threadIdx.x, n, g, ng);
+            __trap();
+        }
+#endif
+        const uint32_t m8 = (hd.w >> sh) & 0xffu;
+        const double w = lane_pairs(rec + 1, n, nb, 0.0);
+        rec += 1 + n;
+#pragma unroll
+        for (int r = 0; r < R; r++) pfma(A[r], w, q[r], m8 & (1u << r));
+    }
+}
+
+// one unit's rate contributions: returns the thread-level W (tile part + lane-only
+// pairs); register-dependent groups are applied to A directly with q
+struct Prog {
+    const uint4 *pg;   // program header; records at pg + V3_HDR16
+    uint32_t has;
+    __device__ __forceinline__ double W0(int u) const { return reinterpret_cast<const double *>(pg + 8)[u]; }
+};
+__device__ __forceinline__ double unit_rates(const Prog &P, int u, uint32_t nb, int sh, double w0,
+                                             const double (&q)[R], double (&A)[R]) {
+    if (!((P.has >> u) & 1u)) return w0;
+    const uint32_t inf = reinterpret_cast<const uint32_t *>(P.pg)[u];
+    const uint4 *p0 = P.pg + V3_HDR16 + (inf >> 16);
+    const int nl = (int)(inf & 0xffu);
+    const double Wt = lane_pairs(p0, nl, nb, w0);
+    const int ng = (int)((inf >> 8) & 0xffu);
+    if (ng) reg_groups(p0 + nl, ng, nb, sh, q, A);
+    return Wt;
 }
 
 // value slots (partial[..][layer][slot]) of the reduced quantities
@@ -110,21 +172,28 @@ struct Slots {
     }
 };
 
+// coalesced read-only 16-byte load of two adjacent states, no L1 allocation
+__device__ __forceinline__ double2 ldg2(const double *p) {
+    double2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    return v;
+}
+
 template <int MODE, bool FULL>
 __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
     using SL = Slots<MODE, FULL>;
     constexpr int NB = SL::NB;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t tbar[2];
-    __shared__ __align__(8) uint64_t rbar[16][RING];
     __shared__ double s_x[32], s_y[32], s_z[32], s_mr[R];
 
     const int nW = a.nW, T = 8 + nW, NVU = 9 + nW, nH = a.N - NVU;
     const int tid = threadIdx.x, lane = tid & 31, warp = wuni(tid >> 5);
-    const uint32_t tstates = 1u << T;
-    double *tileq = reinterpret_cast<double *>(smem_raw);
-    uint4 *progb = reinterpret_cast<uint4 *>(tileq + 2 * tstates);
-    double *ring = reinterpret_cast<double *>(progb + 2 * a.maxrec16) + (size_t)warp * RING * V3_SLOT;
+    const unsigned nwarps = 1u << nW;
+    const uint32_t TS = 1u << T;
+    double *tileq = reinterpret_cast<double *>(smem_raw);                    // [2][TS]
+    uint4 *progb = reinterpret_cast<uint4 *>(tileq + 2 * TS);               // [2][maxblk16]
+    double *fscr = reinterpret_cast<double *>(progb + 2 * a.maxblk16) + (size_t)warp * 32 * 3 * NB;   // flush scratch
 
     if (tid < 32) {
         if (MODE == 2) {
@@ -141,81 +210,40 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
             s_mr[tid] = ((tid & 1) ? a.nu[1] : 0.0) + ((tid & 2) ? a.nu[7] : 0.0) + ((tid & 4) ? a.nu[8] : 0.0);
     }
     if (tid == 0) {
-        mbar_init(&tbar[0], 1);
-        mbar_init(&tbar[1], 1);
+        mbar_init(sptr(&tbar[0]), 1);
+        mbar_init(sptr(&tbar[1]), 1);
     }
-    if (lane < RING) mbar_init(&rbar[warp][lane], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();
 
-    const uint64_t i0 = (uint64_t)blockIdx.x * a.chunk;
-    const uint64_t i1 = min(i0 + a.chunk, a.ntiles);
-    const int nt = i1 > i0 ? (int)(i1 - i0) : 0;
+    // tiles of this CTA: visit indices blockIdx.x + k * gridDim.x (round-robin over the
+    // popcount-sorted order: every CTA sees the same mix of light and heavy tiles)
+    const uint64_t G = gridDim.x;
+    const int nt = blockIdx.x < a.ntiles ? (int)((a.ntiles - 1 - blockIdx.x) / G + 1) : 0;
+    const uint64_t nwt = a.ntiles << nW;   // warp tiles
 
-    // ---- CTA-level tile loader (thread 0): q block of the tile + its rate program
+    // ---- tile loader (thread 0): q block of the tile + the programs of its warp tiles,
+    //      double-buffered; a program block larger than the buffer stays in global memory
     auto load_tile = [&](int k) {
-        const uint64_t idx = i0 + k;
-        const uint32_t t = __ldg(a.order + idx);
-        const uint32_t o = __ldg(a.off16 + idx);
-        const uint32_t nrec = (idx + 1 < a.ntiles ? __ldg(a.off16 + idx + 1) : a.total16) - o;
+        const uint64_t widx = (blockIdx.x + (uint64_t)k * G) << nW;
+        const uint32_t t = __ldg(a.order + widx) >> nW;
+        const uint32_t o = __ldg(a.off16 + widx);
+        const uint32_t nrec = (widx + nwarps < nwt ? __ldg(a.off16 + widx + nwarps) : a.total16) - o;
+        const bool staged = nrec <= a.maxblk16;
         const int buf = k & 1;
-        mbar_expect(&tbar[buf], tstates * 8u + nrec * 16u);
-        bulk_g2s(tileq + (size_t)buf * tstates, a.Q + ((size_t)t << T), tstates * 8u, &tbar[buf]);
-        bulk_g2s(progb + (size_t)buf * a.maxrec16, a.prog + o, nrec * 16u, &tbar[buf]);
+        const unsigned bar = sptr(&tbar[buf]);
+        mbar_expect(bar, TS * 8u + (staged ? nrec * 16u : 0u));
+        bulk_g2s(sptr(tileq + (size_t)buf * TS), a.Q + ((size_t)t << T), TS * 8u, bar);
+        if (staged) bulk_g2s(sptr(progb + (size_t)buf * a.maxblk16), a.prog + o, nrec * 16u, bar);
     };
-
-    // ---- per-warp ring: items of a tile = H-unit neighbour slices [, own p] [, omega/kappa x 2]
-    const int nitems = nH + (MODE >= 1 ? 1 : 0) + (MODE < 2 ? 2 : 0);
-    const int total = nt * nitems;
-    int issued = 0, consumed = 0, pk = 0, pb = 0;
-    uint32_t pt = nt > 0 ? __ldg(a.order + i0) : 0u;
-    const uint32_t wb = (uint32_t)warp << 8;
-    auto issue_next = [&]() {
-        if (lane == 0) {
-            const uint32_t jt = pt << T;
-            const void *src;
-            if (pb < nH) src = a.Q + ((jt ^ (1u << (T + pb))) + wb);
-            else if (MODE >= 1 && pb == nH) src = a.P + (jt + wb);
-            else src = a.omkap + (jt + wb) + 128u * (uint32_t)(pb - nH - (MODE >= 1 ? 1 : 0));
-            const int slot = issued & (RING - 1);
-            fence_proxy_async();
-            mbar_expect(&rbar[warp][slot], V3_SLOT * 8u);
-            bulk_g2s(ring + slot * V3_SLOT, src, V3_SLOT * 8u, &rbar[warp][slot]);
-        }
-        issued++;
-        if (++pb == nitems) {
-            pb = 0;
-            if (++pk < nt) pt = __ldg(a.order + i0 + pk);
-        }
-    };
-    auto produce = [&]() {
-        while (issued < total && issued < consumed + RING) issue_next();
-    };
-    auto wait_at = [&](int ahead) -> const double * {   // item consumed + ahead
-        const int g = consumed + ahead;
-        const int slot = g & (RING - 1);
-        mbar_wait(&rbar[warp][slot], (unsigned)((g / RING) & 1));
-        return ring + slot * V3_SLOT;
-    };
-    auto wait_slot = [&]() -> const double * { return wait_at(0); };
-    auto release_n = [&](int n) {
-        __syncwarp();
-        consumed += n;
-        produce();
-    };
-    auto release = [&]() { release_n(1); };
-
-    produce();
     if (tid == 0 && nt > 0) load_tile(0);
 
     // ---- per-thread constants
-    const uint32_t busy_t = ((uint32_t)lane << 2) | ((uint32_t)warp << 9);   // L units 2..6, W units 9..
+    const uint32_t nb = ~((uint32_t)lane << 2);   // lane units 2..6 busy per lane bit
     double mu_t = 0.0;
 #pragma unroll
     for (int b = 0; b < 5; b++)
         if ((lane >> b) & 1) mu_t += a.nu[2 + b];
-    for (int b = 0; b < nW; b++)
-        if ((warp >> b) & 1) mu_t += a.nu[9 + b];
     const int popc_t = __popc(lane) + __popc(warp);
     const int par_t = popc_t & 1;
     const uint32_t jw = ((uint32_t)warp << 8) | ((uint32_t)lane << 1);   // j_local(r) = jw | (r>>1)<<6 | (r&1)
@@ -231,43 +259,67 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
         for (int v = 0; v < NB; v++) bins[h][v] = 0.0;
     int curK = -1;
 
+    // layer of bin h of this thread at tile popcount K: K + popc_t + beta + 2h.
+    // Flush: lanes write their bins to a per-warp scratch; lane y (< 6 NB) sums, in
+    // lane order, the entries that fall on relative layer y / NB of the warp.
     auto flush = [&]() {
         if (curK < 0) return;
         const int betaK = a.c ^ (curK & 1) ^ par_t;
-        const int Lb = curK + popc_t + betaK;   // layers Lb, Lb + 2, Lb + 4
-        const int L0 = curK + __popc(warp);
-        for (int Lc = L0; Lc <= L0 + 10 && Lc < HQ_NL; Lc++) {
-            if ((Lc & 1) != a.c) continue;
-            const bool any = (Lb == Lc) || (Lb + 2 == Lc) || (Lb + 4 == Lc);
-            if (!__any_sync(0xffffffffu, any)) continue;
-#pragma unroll
-            for (int v = 0; v < NB; v++) {
-                double s = (Lb == Lc ? bins[0][v] : 0.0) + (Lb + 2 == Lc ? bins[1][v] : 0.0) +
-                           (Lb + 4 == Lc ? bins[2][v] : 0.0);
-                s = warp_sum(s);
-                if (lane == Lc) acc[v] += s;
-            }
-        }
+        const int L0 = curK + __popc(warp) + ((a.c ^ curK ^ __popc(warp)) & 1);   // lowest layer of the warp
+        const int z = (popc_t - __popc(warp) + betaK - ((a.c ^ curK ^ __popc(warp)) & 1)) >> 1;   // thread offset
 #pragma unroll
         for (int h = 0; h < 3; h++)
 #pragma unroll
-            for (int v = 0; v < NB; v++) bins[h][v] = 0.0;
+            for (int v = 0; v < NB; v++) fscr[(lane * 3 + h) * NB + v] = bins[h][v];
+        __syncwarp();
+        double s = 0.0;
+        const int y = lane / NB, v = lane - y * NB;   // relative layer (step 2) and value
+        for (int l = 0; l < 32; l++) {
+            const int hh = y - __shfl_sync(0xffffffffu, z, l);
+            if (lane < 6 * NB && hh >= 0 && hh < 3) s += fscr[(l * 3 + hh) * NB + v];
+        }
+        __syncwarp();
+        // move the sums to the lanes that own the layers (lane L holds layer L)
+#pragma unroll
+        for (int yy = 0; yy < 6; yy++)
+#pragma unroll
+            for (int vv = 0; vv < NB; vv++) {
+                const double x = __shfl_sync(0xffffffffu, s, yy * NB + vv);
+                if (lane == L0 + 2 * yy) acc[vv] += x;
+            }
+#pragma unroll
+        for (int h = 0; h < 3; h++)
+#pragma unroll
+            for (int v2 = 0; v2 < NB; v2++) bins[h][v2] = 0.0;
     };
 
     for (int k = 0; k < nt; k++) {
+        const uint64_t widx = (blockIdx.x + (uint64_t)k * G) << nW;
+        const uint32_t t = (uint32_t)wuni((int)(__ldg(a.order + widx) >> nW));
+        const uint32_t jt = t << T;
         const int buf = k & 1;
-        const uint32_t t = (uint32_t)wuni((int)__ldg(a.order + i0 + k));
-        mbar_wait(&tbar[buf], (unsigned)((k >> 1) & 1));
-        __syncthreads();   // every warp is done with tile k-1: its buffer may be refilled
+        // first tile-unit neighbours: in flight while the tile block arrives
+        double2 pre[4];
+        if (nH > 0) {
+            const double *src = a.Q + ((jt ^ (1u << T)) | jw);
+#pragma unroll
+            for (int kk = 0; kk < 4; kk++) pre[kk] = ldg2(src + (kk << 6));
+        }
+        mbar_wait(sptr(&tbar[buf]), (unsigned)((k >> 1) & 1));
+        __syncthreads();   // every warp is done with tile k-1: its buffers may be refilled
         if (tid == 0 && k + 1 < nt) {
             fence_proxy_async();
             load_tile(k + 1);
         }
-        const double *tq = tileq + (size_t)buf * tstates;
-        const uint4 *pg = progb + (size_t)buf * a.maxrec16;
-        const uint32_t *info = reinterpret_cast<const uint32_t *>(pg);
-        const double *W0 = reinterpret_cast<const double *>(pg + 8);
-        const uint4 *pr = pg + V3_HDR16;
+        const double *tq = tileq + (size_t)buf * TS;
+        Prog P;
+        {
+            const uint32_t o0 = __ldg(a.off16 + widx), ow = __ldg(a.off16 + widx + warp);
+            const uint32_t nrec = (widx + nwarps < nwt ? __ldg(a.off16 + widx + nwarps) : a.total16) - o0;
+            const uint4 *pg = nrec <= a.maxblk16 ? progb + (size_t)buf * a.maxblk16 + (ow - o0) : a.prog + ow;
+            P.pg = pg;
+            P.has = pg[24].z;
+        }
         const int K = __popc(t);
         if (K != curK) {
             flush();
@@ -275,9 +327,7 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
         }
         const int beta = a.c ^ (K & 1) ^ par_t;
         const int sh = beta ? 8 : 0;
-        double mu_F = 0.0;
-        for (int h = 0; h < nH; h++)
-            if ((t >> h) & 1u) mu_F += a.nu[NVU + h];
+        const double mu_F = reinterpret_cast<const double *>(P.pg + 24)[0];
 
         double qo[R], A[R], D[R], q[R];
 #pragma unroll
@@ -293,9 +343,7 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
         }
         // ---- unit 0 (implied parity bit): busy in r iff b0(r) = beta ^ parity(r)
         {
-            const uint32_t inf = info[0];
-            const uint4 *p0 = pr + (inf >> 16);
-            const double Wt = lane_pairs(p0, (int)(inf & 0xffu), busy_t, W0[0]);
+            const double Wt = unit_rates(P, 0, nb, sh, P.W0(0), qo, A);
             const double We = beta ? Wt : 0.0, Wo = beta ? 0.0 : Wt;
             const double Ne = beta ? 0.0 : nu0, No = beta ? nu0 : 0.0;
 #pragma unroll
@@ -304,32 +352,26 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
                 A[r] = fma(odd ? Wo : We, qo[r], A[r]);
                 D[r] = fma(odd ? No : Ne, qo[r], D[r]);
             }
-            reg_pairs(p0 + (inf & 0xffu), (int)((inf >> 8) & 0xffu), busy_t, sh, qo, A);
         }
         // ---- register units 1, 7, 8 (register bits 0, 1, 2)
 #pragma unroll
         for (int rb = 0; rb < 3; rb++) {
             const int u = rb ? 6 + rb : 1;
             const int bit = 1 << rb;
-            const uint32_t inf = info[u];
-            const uint4 *p0 = pr + (inf >> 16);
-            const double Wt = lane_pairs(p0, (int)(inf & 0xffu), busy_t, W0[u]);
-            const double nuu = a.nu[u];
 #pragma unroll
             for (int r = 0; r < R; r++) q[r] = qo[r ^ bit];
+            const double Wt = unit_rates(P, u, nb, sh, P.W0(u), q, A);
+            const double nuu = a.nu[u];
 #pragma unroll
             for (int r = 0; r < R; r++) {
                 if (r & bit) A[r] = fma(Wt, q[r], A[r]);
                 else D[r] = fma(nuu, q[r], D[r]);
             }
-            reg_pairs(p0 + (inf & 0xffu), (int)((inf >> 8) & 0xffu), busy_t, sh, q, A);
         }
-        // ---- lane units 2..6 (lane bits 0..4): busy per lane
+        // ---- lane units 2..6 (lane bits 0..4): busy per lane; their pairs carry the own bit
 #pragma unroll
         for (int b = 0; b < 5; b++) {
             const int u = 2 + b;
-            const uint32_t inf = info[u];
-            const uint4 *p0 = pr + (inf >> 16);
             const bool busy = (lane >> b) & 1;
             const uint32_t jn = jw ^ (2u << b);
 #pragma unroll
@@ -338,15 +380,13 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
                 q[2 * kk] = v.x;
                 q[2 * kk + 1] = v.y;
             }
-            // the pairs of a lane unit carry its own bit: they vanish where it is free
-            const double Wt = lane_pairs(p0, (int)(inf & 0xffu), busy_t, busy ? W0[u] : 0.0);
+            const double Wt = unit_rates(P, u, nb, sh, busy ? P.W0(u) : 0.0, q, A);
             const double wn = busy ? 0.0 : a.nu[u];
 #pragma unroll
             for (int r = 0; r < R; r++) {
                 A[r] = fma(Wt, q[r], A[r]);
                 D[r] = fma(wn, q[r], D[r]);
             }
-            reg_pairs(p0 + (inf & 0xffu), (int)((inf >> 8) & 0xffu), busy_t, sh, q, A);
         }
         // ---- warp units 9..8+nW (warp bits): busy per warp (uniform branch)
         for (int b = 0; b < nW; b++) {
@@ -359,75 +399,58 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
                 q[2 * kk + 1] = v.y;
             }
             if ((warp >> b) & 1) {
-                const uint32_t inf = info[u];
-                const uint4 *p0 = pr + (inf >> 16);
-                const double Wt = lane_pairs(p0, (int)(inf & 0xffu), busy_t, W0[u]);
+                const double Wt = unit_rates(P, u, nb, sh, P.W0(u), q, A);
 #pragma unroll
                 for (int r = 0; r < R; r++) A[r] = fma(Wt, q[r], A[r]);
-                reg_pairs(p0 + (inf & 0xffu), (int)((inf >> 8) & 0xffu), busy_t, sh, q, A);
             } else {
                 const double nuu = a.nu[u];
 #pragma unroll
                 for (int r = 0; r < R; r++) D[r] = fma(nuu, q[r], D[r]);
             }
         }
-        // ---- tile units (H): neighbour tile slices from the ring, busy per tile
+        // ---- tile units (H): neighbour tile slices straight from global memory (L2),
+        //      one unit of loads in flight ahead of the unit being accumulated
         for (int h = 0; h < nH; h++) {
             const int u = NVU + h;
-            const double *sl = wait_slot();
 #pragma unroll
             for (int kk = 0; kk < 4; kk++) {
-                const double2 v = *reinterpret_cast<const double2 *>(sl + ((lane << 1) | (kk << 6)));
-                q[2 * kk] = v.x;
-                q[2 * kk + 1] = v.y;
+                q[2 * kk] = pre[kk].x;
+                q[2 * kk + 1] = pre[kk].y;
             }
-            release();
+            if (h + 1 < nH) {
+                const double *src = a.Q + ((jt ^ (1u << (T + h + 1))) | jw);
+#pragma unroll
+                for (int kk = 0; kk < 4; kk++) pre[kk] = ldg2(src + (kk << 6));
+            }
             if ((t >> h) & 1u) {
-                const uint32_t inf = info[u];
-                const uint4 *p0 = pr + (inf >> 16);
-                const double Wt = lane_pairs(p0, (int)(inf & 0xffu), busy_t, W0[u]);
+                const double Wt = unit_rates(P, u, nb, sh, P.W0(u), q, A);
 #pragma unroll
                 for (int r = 0; r < R; r++) A[r] = fma(Wt, q[r], A[r]);
-                reg_pairs(p0 + (inf & 0xffu), (int)((inf >> 8) & 0xffu), busy_t, sh, q, A);
             } else {
                 const double nuu = a.nu[u];
 #pragma unroll
                 for (int r = 0; r < R; r++) D[r] = fma(nuu, q[r], D[r]);
             }
         }
-        // ---- own old p (convergence proxy / residual): read in the epilogue, slot held until then
-        const double *slp = MODE >= 1 ? wait_at(0) : nullptr;
         // ---- lambda_m: Lambda minus the atoms whose whole (truncated) list is busy
         double lam[R];
         if (FULL) {
 #pragma unroll
             for (int r = 0; r < R; r++) lam[r] = a.Lam;
         } else {
-            const int u = a.N;
-            const uint32_t inf = info[u];
-            const uint4 *p0 = pr + (inf >> 16);
-            const double Bt = lane_pairs(p0, (int)(inf & 0xffu), busy_t, W0[u]);
             double one[R];
 #pragma unroll
             for (int r = 0; r < R; r++) {
-                lam[r] = Bt;
+                lam[r] = 0.0;
                 one[r] = 1.0;
             }
-            reg_pairs(p0 + (inf & 0xffu), (int)((inf >> 8) & 0xffu), busy_t, sh, one, lam);
+            const double Bt = unit_rates(P, a.N, nb, sh, P.W0(a.N), one, lam);
 #pragma unroll
-            for (int r = 0; r < R; r++) lam[r] = a.Lam - lam[r];
+            for (int r = 0; r < R; r++) lam[r] = a.Lam - (lam[r] + Bt);
         }
-        // ---- scatter weights omega, kappa of the updated states (two slots, read in the epilogue)
-        const double2 *slo0 = nullptr, *slo1 = nullptr;
-        if (MODE < 2) {
-            const int o = MODE >= 1 ? 1 : 0;
-            slo0 = reinterpret_cast<const double2 *>(wait_at(o));
-            slo1 = reinterpret_cast<const double2 *>(wait_at(o + 1));
-        }
-        // ---- epilogue
+        // ---- epilogue (own old p and scatter weights straight from global memory)
         const int base = K + popc_t;
         const double mu_base = mu_F + mu_t;
-        const uint32_t jt = t << T;
         double pnew[R];
         bool act[R];
 #pragma unroll
@@ -439,10 +462,10 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
             double lm = lam[r];
             if (FULL && n == a.N) lm = 0.0;
             const double den = lm + mu;
+            const uint32_t j = jt + (jw | ((r >> 1) << 6) | (r & 1));
+            const double pold = MODE >= 1 ? __ldg(a.P + j) : 0.0;
             double val[NB];
             act[r] = true;
-            const int so = ((r >> 1) << 6) | (lane << 1) | (r & 1);   // warp-local state offset
-            const double pold = MODE >= 1 ? slp[so] : 0.0;
             if (MODE == 2) {
                 const double out = s_z[n] * pold * den;
                 const double in = s_x[n] * A[r] + s_y[n] * D[r];
@@ -451,7 +474,7 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
             } else {
                 act[r] = (a.active >> n) & 1u;
                 const double p = (s_x[n] * A[r] + s_y[n] * D[r]) * __drcp_rn(den);
-                const double2 ok = (r < 4 ? slo0 : slo1)[so & 127];
+                const double2 ok = __ldg(a.omkap + j);
                 pnew[r] = p;
                 val[0] = act[r] ? p : 0.0;
                 val[1] = act[r] ? p * ok.x : 0.0;
@@ -474,7 +497,6 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
                 }
             }
         }
-        release_n((MODE >= 1 ? 1 : 0) + (MODE < 2 ? 2 : 0));
         if (MODE < 2) {
 #pragma unroll
             for (int kk = 0; kk < 4; kk++) {
@@ -490,18 +512,18 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
     }
     flush();
     // ---- CTA partials: warp w's lane L holds layer L; fixed-order sum over warps
-    __syncwarp();
+    __syncthreads();   // no copy in flight: reuse the tile buffers
+    double *red = tileq;
 #pragma unroll
-    for (int v = 0; v < NB; v++) ring[lane * NB + v] = acc[v];
+    for (int v = 0; v < NB; v++) red[((size_t)warp * 32 + lane) * NB + v] = acc[v];
     __syncthreads();
     if (warp == 0) {
-        const double *base = reinterpret_cast<const double *>(progb + 2 * a.maxrec16);
         double s[NB];
 #pragma unroll
         for (int v = 0; v < NB; v++) s[v] = 0.0;
-        for (int w = 0; w < (1 << nW); w++)
+        for (int w = 0; w < (int)nwarps; w++)
 #pragma unroll
-            for (int v = 0; v < NB; v++) s[v] += base[(size_t)w * RING * V3_SLOT + lane * NB + v];
+            for (int v = 0; v < NB; v++) s[v] += red[((size_t)w * 32 + lane) * NB + v];
         double *out = a.partial + ((size_t)blockIdx.x * HQ_NL + lane) * HQ_NV;
 #pragma unroll
         for (int v = 0; v < HQ_NV; v++) out[v] = 0.0;
@@ -514,12 +536,15 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
 // Rate-program precompute (once per instance): Algorithm 3
 // walked symbolically over the tile's varying units.
 // ---------------------------------------------------------------------------
+constexpr int MAXP = V3_MAXPAIRS;
+constexpr uint32_t PRMASK = 1u | (1u << 1) | (1u << 7) | (1u << 8);   // parity + register units
+
 struct PairAcc3 {
     int n;
-    uint32_t key[V3_MAXPAIRS / 4];   // unit | S << 6
-    double val[V3_MAXPAIRS / 4];
+    uint32_t key[MAXP];   // unit | S << 6
+    double val[MAXP];
+    uint16_t rm[MAXP];
 };
-constexpr int MAXP = V3_MAXPAIRS / 4;
 
 __device__ __forceinline__ bool pair_add3(PairAcc3 &P, double *W0, int u, uint32_t S, double val) {
     if (S == 0u) {
@@ -539,8 +564,32 @@ __device__ __forceinline__ bool pair_add3(PairAcc3 &P, double *W0, int u, uint32
     return true;
 }
 
-__device__ bool tile_walk3(const P3Args &a, uint32_t t, double *W0, PairAcc3 &P) {
-    const int NVU = 9 + a.nW;
+// admissible register states of a register-dependent pair (unit u, pattern S), beta = 0 | 1 << 8
+__device__ uint32_t reg_mask(int u, uint32_t S, bool pseudo) {
+    uint32_t rm = 0u;
+    for (int beta = 0; beta < 2; beta++)
+        for (int r = 0; r < R; r++) {
+            const int b0 = beta ^ (__popc(r) & 1);
+            bool ok = true;
+            if ((S & (1u << 1)) && !(r & 1)) ok = false;
+            if ((S & (1u << 7)) && !(r & 2)) ok = false;
+            if ((S & (1u << 8)) && !(r & 4)) ok = false;
+            if ((S & 1u) && !b0) ok = false;
+            if (!pseudo) {   // own busy condition of the parity / register units
+                if (u == 0 && !b0) ok = false;
+                if (u == 1 && !(r & 1)) ok = false;
+                if (u == 7 && !(r & 2)) ok = false;
+                if (u == 8 && !(r & 4)) ok = false;
+            }
+            if (ok) rm |= 1u << (r + 8 * beta);
+        }
+    return rm;
+}
+
+// Walk the trie for tile t, then sort the pairs by (unit, class, rm).
+// Returns the number of 16-byte records after the header, or -1 on overflow.
+__device__ int tile_program(const P3Args &a, uint32_t t, double *W0, PairAcc3 &P) {
+    const int NVU = 9;
     uint32_t Sst[HQ_MAXN + 2];
     Sst[0] = 0;
     for (int u = 0; u <= HQ_MAXN; u++) W0[u] = 0.0;
@@ -556,15 +605,43 @@ __device__ bool tile_walk3(const P3Args &a, uint32_t t, double *W0, PairAcc3 &P)
         }
         const uint32_t Spre = Sst[d - 1];
         const uint32_t own = u < NVU ? (1u << u) : 0u;
-        if (!pair_add3(P, W0, u, Spre, __ldg(&a.lam_thr[v]))) return false;
+        if (!pair_add3(P, W0, u, Spre, __ldg(&a.lam_thr[v]))) return -1;
         if (!a.full_lists) {
             const double e = __ldg(&a.lam_end[v]);
-            if (e != 0.0 && !pair_add3(P, W0, a.N, Spre | own, e)) return false;
+            if (e != 0.0 && !pair_add3(P, W0, a.N, Spre | own, e)) return -1;
         }
         Sst[d] = Spre | own;
         v++;
     }
-    return true;
+    for (int k = 0; k < P.n; k++) {
+        const int u = (int)(P.key[k] & 63);
+        const uint32_t S = P.key[k] >> 6;
+        P.rm[k] = (S & PRMASK) ? (uint16_t)reg_mask(u, S, u == a.N) : (uint16_t)0;
+    }
+    // stable insertion sort by (unit, class, rm); lane-only pairs have rm = 0
+    auto rank = [&](int k) -> uint64_t {
+        return ((uint64_t)(P.key[k] & 63) << 20) | ((uint64_t)(P.rm[k] ? 1 : 0) << 16) | P.rm[k];
+    };
+    for (int x = 1; x < P.n; x++) {
+        const uint32_t kx = P.key[x];
+        const double vx = P.val[x];
+        const uint16_t mx = P.rm[x];
+        const uint64_t rx = rank(x);
+        int y = x - 1;
+        while (y >= 0 && rank(y) > rx) {
+            P.key[y + 1] = P.key[y];
+            P.val[y + 1] = P.val[y];
+            P.rm[y + 1] = P.rm[y];
+            y--;
+        }
+        P.key[y + 1] = kx;
+        P.val[y + 1] = vx;
+        P.rm[y + 1] = mx;
+    }
+    int nrec = P.n;
+    for (int k = 0; k < P.n; k++)   // one header per group
+        if (P.rm[k] && (k == 0 || P.rm[k - 1] != P.rm[k] || (P.key[k - 1] & 63) != (P.key[k] & 63))) nrec++;
+    return nrec;
 }
 
 __global__ void k_prog_count3(P3Args a, const uint32_t *__restrict__ order, uint32_t *__restrict__ size16,
@@ -573,93 +650,83 @@ __global__ void k_prog_count3(P3Args a, const uint32_t *__restrict__ order, uint
     double W0[HQ_MAXN + 1];
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.ntiles;
          i += (uint64_t)gridDim.x * blockDim.x) {
-        if (!tile_walk3(a, order[i], W0, P)) {
+        const int nrec = tile_program(a, order[i], W0, P);
+        if (nrec < 0 || nrec >= 65536) {
             atomicExch(err, 2);
             size16[i] = V3_HDR16;
             continue;
         }
-        int cnt[HQ_MAXN + 1][2];
-        for (int u = 0; u <= HQ_MAXN; u++) cnt[u][0] = cnt[u][1] = 0;
-        const uint32_t PR = 1u | (1u << 1) | (1u << 7) | (1u << 8);
-        for (int k = 0; k < P.n; k++) cnt[P.key[k] & 63][((P.key[k] >> 6) & PR) ? 1 : 0]++;
-        for (int u = 0; u <= HQ_MAXN; u++)
-            if (cnt[u][0] > 255 || cnt[u][1] > 255) atomicExch(err, 3);
-        size16[i] = V3_HDR16 + (uint32_t)P.n;
+        size16[i] = V3_HDR16 + (uint32_t)nrec;
     }
 }
 
 __global__ void k_prog_write3(P3Args a, const uint32_t *__restrict__ order, const uint32_t *__restrict__ off16,
-                              uint4 *__restrict__ prog) {
+                              uint4 *__restrict__ prog, int *__restrict__ err) {
     PairAcc3 P;
     double W0[HQ_MAXN + 1];
-    const int NVU = 9 + a.nW;
-    const uint32_t PR = 1u | (1u << 1) | (1u << 7) | (1u << 8);
+    const int NVU = 9;
     uint32_t LW = 0;
     for (int u = 2; u <= 6; u++) LW |= 1u << u;
-    for (int u = 9; u < NVU; u++) LW |= 1u << u;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.ntiles;
          i += (uint64_t)gridDim.x * blockDim.x) {
         uint4 *out = prog + off16[i];
-        if (!tile_walk3(a, order[i], W0, P)) continue;
-        // stable insertion sort by (unit, class): class 0 = lane-only, 1 = register-dependent
-        auto rank = [&](uint32_t key) -> int { return (int)(key & 63) * 2 + ((((key >> 6) & PR) != 0u) ? 1 : 0); };
-        for (int x = 1; x < P.n; x++) {
-            const uint32_t kx = P.key[x];
-            const double vx = P.val[x];
-            const int rx = rank(kx);
-            int y = x - 1;
-            while (y >= 0 && rank(P.key[y]) > rx) {
-                P.key[y + 1] = P.key[y];
-                P.val[y + 1] = P.val[y];
-                y--;
-            }
-            P.key[y + 1] = kx;
-            P.val[y + 1] = vx;
-        }
+        const uint32_t t = order[i];
+        if (tile_program(a, t, W0, P) < 0) continue;
         uint32_t info[32];
         for (int q = 0; q < 32; q++) info[q] = 0u;
-        for (int k = P.n - 1; k >= 0; k--) {   // start = index of the unit's first pair
+        // emit records unit by unit
+        uint32_t pos = 0;   // record index after the header
+        int k = 0;
+        while (k < P.n) {
             const int u = (int)(P.key[k] & 63);
-            info[u] = (info[u] & 0xffffu) | ((uint32_t)k << 16);
+            uint32_t nl = 0, ng = 0;
+            const uint32_t start = pos;
+            while (k < P.n && (int)(P.key[k] & 63) == u) {
+                const uint32_t S = P.key[k] >> 6;
+                const bool pseudo = (u == a.N);
+                uint32_t St = S & LW;
+                if (!pseudo && ((LW >> u) & 1u)) St |= 1u << u;   // lane/warp unit: own busy condition
+                const double c = P.val[k];
+                const uint4 rec = make_uint4((uint32_t)__double_as_longlong(c),
+                                             (uint32_t)((unsigned long long)__double_as_longlong(c) >> 32), St, 0u);
+                if (P.rm[k] == 0) {
+                    out[V3_HDR16 + pos++] = rec;
+                    nl++;
+                    k++;
+                    continue;
+                }
+                // group of equal rm: header then pairs
+                const uint16_t rm = P.rm[k];
+                const uint32_t hpos = pos++;
+                uint32_t cnt = 0;
+                while (k < P.n && (int)(P.key[k] & 63) == u && P.rm[k] == rm) {
+                    const uint32_t S2 = P.key[k] >> 6;
+                    uint32_t St2 = S2 & LW;
+                    if (!pseudo && ((LW >> u) & 1u)) St2 |= 1u << u;
+                    const double c2 = P.val[k];
+                    out[V3_HDR16 + pos++] = make_uint4((uint32_t)__double_as_longlong(c2),
+                                                       (uint32_t)((unsigned long long)__double_as_longlong(c2) >> 32),
+                                                       St2, 0u);
+                    cnt++;
+                    k++;
+                }
+                out[V3_HDR16 + hpos] = make_uint4(0u, 0u, cnt, (uint32_t)rm);
+                ng++;
+            }
+            if (nl > 255 || ng > 255) atomicExch(err, 3);
+            info[u] = nl | (ng << 8) | (start << 16);
         }
-        for (int k = 0; k < P.n; k++) {
-            const int u = (int)(P.key[k] & 63);
-            const bool reg = ((P.key[k] >> 6) & PR) != 0u;
-            info[u] += reg ? (1u << 8) : 1u;
-        }
+        uint32_t has = 0;
+        for (int q = 0; q < 32; q++)
+            if (info[q]) has |= 1u << q;
         for (int q = 0; q < 8; q++) out[q] = make_uint4(info[4 * q], info[4 * q + 1], info[4 * q + 2], info[4 * q + 3]);
         double *w0o = reinterpret_cast<double *>(out + 8);
         for (int u = 0; u < 32; u++) w0o[u] = u <= HQ_MAXN ? W0[u] : 0.0;
-        for (int k = 0; k < P.n; k++) {
-            const int u = (int)(P.key[k] & 63);
-            const uint32_t S = P.key[k] >> 6;
-            const bool pseudo = (u == a.N);
-            uint32_t St = S & LW;
-            if (!pseudo && ((LW >> u) & 1u)) St |= 1u << u;   // lane/warp unit: own busy condition
-            uint32_t rm = 0xffffu;
-            if ((S & PR) != 0u) {
-                rm = 0u;
-                for (int beta = 0; beta < 2; beta++)
-                    for (int r = 0; r < R; r++) {
-                        const int b0 = beta ^ (__popc(r) & 1);
-                        bool ok = true;
-                        if ((S & (1u << 1)) && !(r & 1)) ok = false;
-                        if ((S & (1u << 7)) && !(r & 2)) ok = false;
-                        if ((S & (1u << 8)) && !(r & 4)) ok = false;
-                        if ((S & 1u) && !b0) ok = false;
-                        if (!pseudo) {   // own busy condition of the parity / register units
-                            if (u == 0 && !b0) ok = false;
-                            if (u == 1 && !(r & 1)) ok = false;
-                            if (u == 7 && !(r & 2)) ok = false;
-                            if (u == 8 && !(r & 4)) ok = false;
-                        }
-                        if (ok) rm |= 1u << (r + 8 * beta);
-                    }
-            }
-            const double c = P.val[k];
-            out[V3_HDR16 + k] = make_uint4((uint32_t)__double_as_longlong(c),
-                                           (uint32_t)((unsigned long long)__double_as_longlong(c) >> 32), St, rm);
-        }
+        double muF = 0.0;
+        for (int u = NVU; u < a.N; u++)
+            if ((t >> (u - NVU)) & 1u) muF += a.nu[u];
+        out[24] = make_uint4((uint32_t)__double_as_longlong(muF),
+                             (uint32_t)((unsigned long long)__double_as_longlong(muF) >> 32), has, 0u);
     }
 }
 
@@ -676,24 +743,28 @@ int choose_nw(int N) {
     return nw;
 }
 
-size_t sweep_smem(int nW, uint32_t maxrec16) {
-    const size_t tstates = (size_t)1 << (8 + nW);
-    return 2 * tstates * 8 + 2 * (size_t)maxrec16 * 16 + ((size_t)1 << nW) * V3_RING * V3_SLOT * 8;
+size_t sweep_smem(int nW, uint32_t maxblk16, int nslots) {
+    (void)nslots;
+    const size_t TS = (size_t)1 << (8 + nW);
+    // tile blocks, program blocks, per-warp flush scratch (32 lanes x 3 bins x 5 values)
+    return 2 * TS * 8 + 2 * (size_t)maxblk16 * 16 + ((size_t)1 << nW) * 32 * 3 * 5 * 8;
 }
+
+int choose_slots(int nW, uint32_t maxblk16) { return sweep_smem(nW, maxblk16, 0) <= 224u * 1024u ? 1 : 0; }
 
 cudaError_t prog_count(const P3Args &a, const uint32_t *order, uint32_t *size16, int *err, int grid, cudaStream_t s) {
     hq3::k_prog_count3<<<grid, 64, 0, s>>>(a, order, size16, err);
     return cudaGetLastError();
 }
-cudaError_t prog_write(const P3Args &a, const uint32_t *order, const uint32_t *off16, uint4 *prog, int grid,
-                       cudaStream_t s) {
-    hq3::k_prog_write3<<<grid, 64, 0, s>>>(a, order, off16, prog);
+cudaError_t prog_write(const P3Args &a, const uint32_t *order, const uint32_t *off16, uint4 *prog, int *err,
+                       int grid, cudaStream_t s) {
+    hq3::k_prog_write3<<<grid, 64, 0, s>>>(a, order, off16, prog, err);
     return cudaGetLastError();
 }
 
 template <int MODE, bool FULL>
 static cudaError_t launch(const S3Args &a, int grid, cudaStream_t s) {
-    const size_t sm = sweep_smem(a.nW, a.maxrec16);
+    const size_t sm = sweep_smem(a.nW, a.maxblk16, a.nslots);
     cudaError_t e = cudaFuncSetAttribute(hq3::k_sweep3<MODE, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
     hq3::k_sweep3<MODE, FULL><<<grid, 32 << a.nW, sm, s>>>(a);

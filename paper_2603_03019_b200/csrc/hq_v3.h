@@ -10,23 +10,29 @@
 // Internal unit 0 is the implied parity unit: b0 = c ^ parity(j).
 // A CTA of 32 << nW threads owns one tile (2^T compressed states) at a time;
 // thread (warp w, lane l) owns the 8 states r = 0..7 of its (w, l) slot.
+// Rate programs are per warp tile (256 states, index t' = t << nW | w): only
+// units 0..8 vary inside a program; units >= 9 are fixed by t'.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
 #include "hq_internal.h"
 
 #define V3_R 8                 // states per thread
-#define V3_RING 4              // per-warp ring slots (2 KB each)
-#define V3_SLOT 256            // doubles per ring slot (one warp's 256 states)
-#define V3_HDR16 24            // program header: info[32] (u32) + W0[32] (f64) = 24 x 16 B
-#define V3_MAXPAIRS 4096
+#define V3_MAXSLOTS 8          // CTA ring slots (one tile-sized block each)
+#define V3_HDR16 25            // program header: info[32] (u32), W0[32] (f64), {mu_F, 0}
+#define V3_MAXPAIRS 1024
 
-// program record (16-byte units):
-//   [0..7]   info[u] = n_lane | n_reg << 8 | start << 16   (u = 0..N; N = blocked pseudo-unit)
-//   [8..23]  W0[u] (f64)
-//   pairs    uint4 {c.lo, c.hi, S_t, rm}: S_t = thread-level condition (unit bits of the
-//            lane/warp units that must be busy), rm = admissible register states for
-//            beta = 0 (bits 0..7) and beta = 1 (bits 8..15); lane-only pairs first.
+// program record of a warp tile (16-byte units):
+//   [0..7]   info[u] = n_lane | n_group << 8 | start << 16   (u = 0..N; N = blocked pseudo-unit)
+//   [8..23]  W0[u] (f64): warp-tile-uniform rate part of unit u
+//   [24]     {mu_F (f64), has, 0}: mu_F = sum of nu over the busy units >= 9;
+//            has = bit u set iff unit u has pairs (info[u] != 0)
+//   records  per unit: n_lane lane-only pairs {c.lo, c.hi, S_t, 0}, then n_group groups,
+//            each a header {0, 0, count, rm} followed by count pairs {c.lo, c.hi, S_t, 0}.
+//            S_t = unit bits of the lane units that must be busy (thread-level
+//            condition); rm = admissible register states for beta = 0 (bits 0..7) and
+//            beta = 1 (bits 8..15) of every pair of the group.
+// The programs of the 2^nW warp tiles of a CTA tile are stored contiguously.
 
 struct S3Args {
     int N;
@@ -37,11 +43,12 @@ struct S3Args {
     uint64_t chunk;          // tiles per CTA (contiguous range of the visit order)
     double Lam;
     double nu[32];           // internal-order service rates
-    const uint32_t *order;   // tile visit order
-    const uint32_t *off16;   // program offset of visit index i (16-byte units)
+    const uint32_t *order;   // warp-tile visit order: entry i << nW | w = (t << nW) | w
+    const uint32_t *off16;   // program offset of warp-tile visit index (16-byte units)
     const uint4 *prog;
     uint32_t total16;
-    uint32_t maxrec16;       // largest program (16-byte units)
+    uint32_t maxblk16;       // largest program block of a CTA tile (16-byte units)
+    int nslots;              // CTA ring slots
     const double *Q;         // neighbour class (read)
     double *P;               // updated class (sweep) / evaluated class (residual)
     const double2 *omkap;    // scatter weights of class c
@@ -49,11 +56,11 @@ struct S3Args {
     double *partial;         // [grid][HQ_NL][HQ_NV]
 };
 
-struct P3Args {   // program precompute
+struct P3Args {   // program precompute (per warp tile)
     int N;
-    int nW;
     int full_lists;
     uint64_t ntiles;
+    double nu[32];           // internal-order service rates (mu_F in the header)
     int nnodes;
     const int2 *node;        // .x = unit | depth << 8, .y = skip
     const double *lam_thr;
@@ -62,9 +69,10 @@ struct P3Args {   // program precompute
 
 namespace hq3_launch {
 cudaError_t prog_count(const P3Args &a, const uint32_t *order, uint32_t *size16, int *err, int grid, cudaStream_t s);
-cudaError_t prog_write(const P3Args &a, const uint32_t *order, const uint32_t *off16, uint4 *prog, int grid,
-                       cudaStream_t s);
+cudaError_t prog_write(const P3Args &a, const uint32_t *order, const uint32_t *off16, uint4 *prog, int *err,
+                       int grid, cudaStream_t s);
 cudaError_t sweep(const S3Args &a, int full, int mode, int grid, cudaStream_t s);
-size_t sweep_smem(int nW, uint32_t maxrec16);
+size_t sweep_smem(int nW, uint32_t maxblk16, int nslots);
+int choose_slots(int nW, uint32_t maxblk16);
 int choose_nw(int N);
 }  // namespace hq3_launch
