@@ -314,7 +314,7 @@ struct hq_problem {
     int path = 1;                  // 1: N < 8 two-pass, 2: warp-tiled (hq_v2.cu), 3: CTA-tiled (hq_v3.cu)
     int nW = 0;                    // path 3: log2(warps per CTA)
     int nslots = 0;                // path 3: CTA ring slots
-    uint32_t *d_order = nullptr, *d_off16 = nullptr, *d_size16 = nullptr;
+    uint32_t *d_order = nullptr, *d_off16 = nullptr, *d_size16 = nullptr, *d_range = nullptr;
     uint4 *d_prog = nullptr;
     double2 *d_omkap = nullptr;
     double *d_lamarr = nullptr;
@@ -349,6 +349,8 @@ struct hq_problem {
         cudaFree(d_small);
         cudaFree(d_err);
         cudaFree(d_order);
+        cudaFree(d_range);
+        d_range = nullptr;
         cudaFree(d_off16);
         cudaFree(d_size16);
         cudaFree(d_prog);
@@ -674,24 +676,40 @@ static hq_status v2_prepare(hq_problem *h, cudaStream_t s) {
     HQ_CUDA(cudaMemcpyAsync(&last[1], h->d_size16 + nprog - 1, 4, cudaMemcpyDeviceToHost, s));
     HQ_CUDA(cudaMemcpyAsync(&herr, h->d_err, sizeof(int), cudaMemcpyDeviceToHost, s));
     HQ_CUDA(cudaStreamSynchronize(s));
-    if (nWp) {   // largest program block of a CTA tile
+    if (h->path == 3) {   // program block sizes -> largest block, and work-balanced CTA ranges
         std::vector<uint32_t> sz(nprog);
         HQ_CUDA(cudaMemcpy(sz.data(), h->d_size16, 4 * nprog, cudaMemcpyDeviceToHost));
         uint32_t mb = 0;
+        std::vector<double> cost(ntiles);
+        double tot = 0.0;
         for (uint64_t i = 0; i < ntiles; i++) {
             uint32_t b = 0;
             for (uint32_t x = 0; x < (1u << nWp); x++) b += sz[(i << nWp) | x];
             mb = std::max(mb, b);
+            // estimated work of a tile in program-record units: the gather of its 2^(8+nW)
+            // states (~2048 records' worth at 16 warps) plus one record per program record
+            cost[i] = (double)(128u << nWp) + (double)b;
+            tot += cost[i];
         }
         h->maxrec = mb;
+        const int G = h->sgrid;
+        std::vector<uint32_t> range(G + 1, (uint32_t)ntiles);
+        range[0] = 0;
+        double acc = 0.0;
+        int b = 1;
+        for (uint64_t i = 0; i < ntiles && b < G; i++) {
+            acc += cost[i];
+            while (b < G && acc >= tot * b / G) range[b++] = (uint32_t)(i + 1);
+        }
+        cudaFree(h->d_range);
+        h->d_range = nullptr;
+        HQ_CUDA(cudaMalloc((void **)&h->d_range, 4 * (G + 1)));
+        HQ_CUDA(cudaMemcpy(h->d_range, range.data(), 4 * (G + 1), cudaMemcpyHostToDevice));
     }
     cudaFree(tmp);
     cudaFree(tmp2);
     cudaFree(d_max);
-    if (h->path == 3) {   // staged program capacity: <= 16 KB per buffer; larger blocks stay in global memory
-        h->maxrec = std::min<uint32_t>(h->maxrec, 2048u);
-        h->nslots = hq3_launch::choose_slots(h->nW, h->maxrec);
-    }
+    if (h->path == 3) h->nslots = hq3_launch::choose_slots(h->nW, h->maxrec);
     if (h->path == 3 ? h->nslots < 1 : hq2_launch::sweep_smem(h->maxrec) > 150u * 1024u) {
         h->err = "rate program of a tile exceeds the shared-memory budget";
         return HQ_E_NUMERIC;
@@ -749,6 +767,7 @@ static cudaError_t tiled_sweep(hq_problem *h, const S2Args &sa, int mode, cudaSt
     a.total16 = sa.total16;
     a.maxblk16 = sa.maxrec;
     a.nslots = h->nslots;
+    a.range = h->d_range;
     a.Q = sa.Q;
     a.P = sa.P;
     a.omkap = sa.omkap;

@@ -35,6 +35,7 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdio>
+#include <algorithm>
 #include "hq_internal.h"
 #include "hq_v2.h"
 #include "hq_v3.h"
@@ -110,56 +111,35 @@ __device__ __forceinline__ void padd(double &W, const uint4 &x, uint32_t nb) {
         : "r"(x.x), "r"(x.y), "r"(x.z), "r"(nb));
 }
 
-// tile-uniform part plus the lane-only pairs whose thread-level condition holds
-// (two interleaved partial sums for ILP; fixed order)
-__device__ __forceinline__ double lane_pairs(const uint4 *__restrict__ rec, int n, uint32_t nb, double W) {
-    double W2 = 0.0;
-    int k = 0;
-    for (; k + 1 < n; k += 2) {
-        const uint4 x = rec[k], y = rec[k + 1];
-        padd(W, x, nb);
-        padd(W2, y, nb);
+// Rate program of a warp tile (hq_v3.h): per unit either nothing (the warp-tile-uniform
+// rate W0[u] applies to every lane) or a data block with a per-lane table of the
+// thread-level rate (W0 plus the lane-conditioned pairs, summed at precompute time) and
+// groups of register-dependent pairs, each a mask of admissible register states and a
+// per-lane table of their summed rate.
+struct Prog {
+    const uint4 *__restrict__ pg;   // header (global memory, read through L1)
+    uint32_t info;                  // info[lane] (broadcast to the unit being processed by shuffles)
+    double w0;                      // W0[lane]
+    __device__ __forceinline__ double W0(int u) const { return __shfl_sync(0xffffffffu, w0, u); }
+};
+__device__ __forceinline__ double unit_rates(const Prog &P, int u, int lane, int sh, double w0,
+                                             const double (&q)[R], double (&A)[R]) {
+    const uint32_t inf = __shfl_sync(0xffffffffu, P.info, u);
+    if (!inf) return w0;
+    const uint4 *d = P.pg + V3_HDR16 + ((inf >> 8) & 0xffffu);
+    double Wt = w0;
+    if (inf >> 31) {
+        Wt = __ldg(reinterpret_cast<const double *>(d) + lane);
+        d += 16;
     }
-    if (k < n) padd(W, rec[k], nb);
-    return W + W2;
-}
-
-// register-dependent groups: A[r] += w_g q[r] for the admissible states r of group g
-__device__ __forceinline__ void reg_groups(const uint4 *__restrict__ rec, int ng, uint32_t nb, int sh,
-                                           const double (&q)[R], double (&A)[R]) {
+    const int ng = (int)(inf & 0xffu);
     for (int g = 0; g < ng; g++) {
-        const uint4 hd = rec[0];
-        const int n = (int)hd.z;
-#ifdef HQ_DEBUG_HANG
-        if (n > V3_MAXPAIRS) {
-            printf("hq3 corrupt group: block %d thread %d n %d g %d/%d\n", blockIdx.x, threadIdx.x, n, g, ng);
-            __trap();
-        }
-#endif
-        const uint32_t m8 = (hd.w >> sh) & 0xffu;
-        const double w = lane_pairs(rec + 1, n, nb, 0.0);
-        rec += 1 + n;
+        const uint32_t m8 = (__ldg(&d->x) >> sh) & 0xffu;
+        const double w = __ldg(reinterpret_cast<const double *>(d + 1) + lane);
+        d += 17;
 #pragma unroll
         for (int r = 0; r < R; r++) pfma(A[r], w, q[r], m8 & (1u << r));
     }
-}
-
-// one unit's rate contributions: returns the thread-level W (tile part + lane-only
-// pairs); register-dependent groups are applied to A directly with q
-struct Prog {
-    const uint4 *pg;   // program header; records at pg + V3_HDR16
-    uint32_t has;
-    __device__ __forceinline__ double W0(int u) const { return reinterpret_cast<const double *>(pg + 8)[u]; }
-};
-__device__ __forceinline__ double unit_rates(const Prog &P, int u, uint32_t nb, int sh, double w0,
-                                             const double (&q)[R], double (&A)[R]) {
-    if (!((P.has >> u) & 1u)) return w0;
-    const uint32_t inf = reinterpret_cast<const uint32_t *>(P.pg)[u];
-    const uint4 *p0 = P.pg + V3_HDR16 + (inf >> 16);
-    const int nl = (int)(inf & 0xffu);
-    const double Wt = lane_pairs(p0, nl, nb, w0);
-    const int ng = (int)((inf >> 8) & 0xffu);
-    if (ng) reg_groups(p0 + nl, ng, nb, sh, q, A);
     return Wt;
 }
 
@@ -171,6 +151,27 @@ struct Slots {
         return MODE == 2 ? v : (v < 3 ? v : (!FULL && v == 3) ? V2_LAM : V2_DL1);
     }
 };
+
+// 1/x for x > 0: hardware seed (MUFU.RCP64H) refined by two Newton steps; the result
+// is within 1 ulp of the correctly rounded reciprocal
+__device__ __forceinline__ double rcp_nr(double x) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    double e = fma(-x, y, 1.0);
+    y = fma(y, e, y);
+    e = fma(-x, y, 1.0);
+    return fma(y, e, y);
+}
+// streamed (read-once) 16-byte load, evicted first from L2
+__device__ __forceinline__ double2 ldg_ef(const double2 *p) {
+    double2 v;
+    asm volatile(
+        "{\n\t.reg .b64 pol;\n\tcreatepolicy.fractional.L2::evict_first.b64 pol, 1.0;\n\t"
+        "ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], pol;\n\t}"
+        : "=d"(v.x), "=d"(v.y)
+        : "l"(p));
+    return v;
+}
 
 // coalesced read-only 16-byte load of two adjacent states, no L1 allocation
 __device__ __forceinline__ double2 ldg2(const double *p) {
@@ -192,8 +193,7 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
     const unsigned nwarps = 1u << nW;
     const uint32_t TS = 1u << T;
     double *tileq = reinterpret_cast<double *>(smem_raw);                    // [2][TS]
-    uint4 *progb = reinterpret_cast<uint4 *>(tileq + 2 * TS);               // [2][maxblk16]
-    double *fscr = reinterpret_cast<double *>(progb + 2 * a.maxblk16) + (size_t)warp * 32 * 3 * NB;   // flush scratch
+    double *fscr = tileq + 2 * TS + (size_t)warp * 32 * 3;                  // per-warp flush scratch
 
     if (tid < 32) {
         if (MODE == 2) {
@@ -216,30 +216,32 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();
 
-    // tiles of this CTA: visit indices blockIdx.x + k * gridDim.x (round-robin over the
-    // popcount-sorted order: every CTA sees the same mix of light and heavy tiles)
-    const uint64_t G = gridDim.x;
-    const int nt = blockIdx.x < a.ntiles ? (int)((a.ntiles - 1 - blockIdx.x) / G + 1) : 0;
-    const uint64_t nwt = a.ntiles << nW;   // warp tiles
+    // tiles of this CTA: a contiguous range of the popcount-sorted visit order, cut by the
+    // host so that every CTA gets the same estimated work (few layer flushes, no stragglers)
+    const uint32_t i0 = __ldg(a.range + blockIdx.x), i1 = __ldg(a.range + blockIdx.x + 1);
+    const int nt = (int)(i1 - i0);
 
-    // ---- tile loader (thread 0): q block of the tile + the programs of its warp tiles,
-    //      double-buffered; a program block larger than the buffer stays in global memory
+    // ---- tile loader (thread 0): q block of the tile, double-buffered
     auto load_tile = [&](int k) {
-        const uint64_t widx = (blockIdx.x + (uint64_t)k * G) << nW;
-        const uint32_t t = __ldg(a.order + widx) >> nW;
-        const uint32_t o = __ldg(a.off16 + widx);
-        const uint32_t nrec = (widx + nwarps < nwt ? __ldg(a.off16 + widx + nwarps) : a.total16) - o;
-        const bool staged = nrec <= a.maxblk16;
+        const uint32_t t = __ldg(a.order + ((uint64_t)(i0 + k) << nW)) >> nW;
         const int buf = k & 1;
         const unsigned bar = sptr(&tbar[buf]);
-        mbar_expect(bar, TS * 8u + (staged ? nrec * 16u : 0u));
+        mbar_expect(bar, TS * 8u);
         bulk_g2s(sptr(tileq + (size_t)buf * TS), a.Q + ((size_t)t << T), TS * 8u, bar);
-        if (staged) bulk_g2s(sptr(progb + (size_t)buf * a.maxblk16), a.prog + o, nrec * 16u, bar);
+    };
+    // ---- program prefetch: this warp's program of tile k into L1
+    auto prefetch_prog = [&](int k) {
+        const uint64_t widx = ((uint64_t)(i0 + k) << nW) + warp;
+        const uint32_t o = __ldg(a.off16 + widx);
+        const uint32_t e = widx + 1 < ((uint64_t)a.ntiles << nW) ? __ldg(a.off16 + widx + 1) : a.total16;
+        const char *b = reinterpret_cast<const char *>(a.prog + o);
+        const uint32_t nl = ((e - o) * 16u + 127u) / 128u + 1u;
+        for (uint32_t x = lane; x < nl; x += 32) asm volatile("prefetch.global.L1 [%0];" ::"l"(b + 128 * (size_t)x));
     };
     if (tid == 0 && nt > 0) load_tile(0);
+    if (nt > 0) prefetch_prog(0);
 
     // ---- per-thread constants
-    const uint32_t nb = ~((uint32_t)lane << 2);   // lane units 2..6 busy per lane bit
     double mu_t = 0.0;
 #pragma unroll
     for (int b = 0; b < 5; b++)
@@ -265,36 +267,35 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
     auto flush = [&]() {
         if (curK < 0) return;
         const int betaK = a.c ^ (curK & 1) ^ par_t;
-        const int L0 = curK + __popc(warp) + ((a.c ^ curK ^ __popc(warp)) & 1);   // lowest layer of the warp
-        const int z = (popc_t - __popc(warp) + betaK - ((a.c ^ curK ^ __popc(warp)) & 1)) >> 1;   // thread offset
+        const int p0 = (a.c ^ curK ^ __popc(warp)) & 1;
+        const int L0 = curK + __popc(warp) + p0;                   // lowest layer of the warp
+        const int z = (popc_t - __popc(warp) + betaK - p0) >> 1;   // this lane's bins sit at L0 + 2 (z + h)
+        const int y = lane;                                        // lanes 0..5: relative layer L0 + 2y
 #pragma unroll
-        for (int h = 0; h < 3; h++)
+        for (int v = 0; v < NB; v++) {
 #pragma unroll
-            for (int v = 0; v < NB; v++) fscr[(lane * 3 + h) * NB + v] = bins[h][v];
-        __syncwarp();
-        double s = 0.0;
-        const int y = lane / NB, v = lane - y * NB;   // relative layer (step 2) and value
-        for (int l = 0; l < 32; l++) {
-            const int hh = y - __shfl_sync(0xffffffffu, z, l);
-            if (lane < 6 * NB && hh >= 0 && hh < 3) s += fscr[(l * 3 + hh) * NB + v];
-        }
-        __syncwarp();
-        // move the sums to the lanes that own the layers (lane L holds layer L)
-#pragma unroll
-        for (int yy = 0; yy < 6; yy++)
-#pragma unroll
-            for (int vv = 0; vv < NB; vv++) {
-                const double x = __shfl_sync(0xffffffffu, s, yy * NB + vv);
-                if (lane == L0 + 2 * yy) acc[vv] += x;
+            for (int h = 0; h < 3; h++) fscr[lane * 3 + h] = bins[h][v];
+            __syncwarp();
+            double s = 0.0;
+            for (int l = 0; l < 32; l++) {   // fixed lane order
+                const int hh = y - __shfl_sync(0xffffffffu, z, l);
+                if (y < 6 && hh >= 0 && hh < 3) s += fscr[l * 3 + hh];
             }
+            __syncwarp();
+#pragma unroll
+            for (int yy = 0; yy < 6; yy++) {
+                const double x = __shfl_sync(0xffffffffu, s, yy);
+                if (lane == L0 + 2 * yy) acc[v] += x;
+            }
+        }
 #pragma unroll
         for (int h = 0; h < 3; h++)
 #pragma unroll
-            for (int v2 = 0; v2 < NB; v2++) bins[h][v2] = 0.0;
+            for (int v = 0; v < NB; v++) bins[h][v] = 0.0;
     };
 
     for (int k = 0; k < nt; k++) {
-        const uint64_t widx = (blockIdx.x + (uint64_t)k * G) << nW;
+        const uint64_t widx = (uint64_t)(i0 + k) << nW;
         const uint32_t t = (uint32_t)wuni((int)(__ldg(a.order + widx) >> nW));
         const uint32_t jt = t << T;
         const int buf = k & 1;
@@ -311,15 +312,12 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
             fence_proxy_async();
             load_tile(k + 1);
         }
+        if (k + 1 < nt) prefetch_prog(k + 1);
         const double *tq = tileq + (size_t)buf * TS;
         Prog P;
-        {
-            const uint32_t o0 = __ldg(a.off16 + widx), ow = __ldg(a.off16 + widx + warp);
-            const uint32_t nrec = (widx + nwarps < nwt ? __ldg(a.off16 + widx + nwarps) : a.total16) - o0;
-            const uint4 *pg = nrec <= a.maxblk16 ? progb + (size_t)buf * a.maxblk16 + (ow - o0) : a.prog + ow;
-            P.pg = pg;
-            P.has = pg[24].z;
-        }
+        P.pg = a.prog + __ldg(a.off16 + widx + warp);
+        P.info = __ldg(reinterpret_cast<const uint32_t *>(P.pg) + lane);
+        P.w0 = __ldg(reinterpret_cast<const double *>(P.pg + 8) + lane);
         const int K = __popc(t);
         if (K != curK) {
             flush();
@@ -327,7 +325,7 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
         }
         const int beta = a.c ^ (K & 1) ^ par_t;
         const int sh = beta ? 8 : 0;
-        const double mu_F = reinterpret_cast<const double *>(P.pg + 24)[0];
+        const double mu_F = __ldg(reinterpret_cast<const double *>(P.pg + 24));
 
         double qo[R], A[R], D[R], q[R];
 #pragma unroll
@@ -343,7 +341,7 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
         }
         // ---- unit 0 (implied parity bit): busy in r iff b0(r) = beta ^ parity(r)
         {
-            const double Wt = unit_rates(P, 0, nb, sh, P.W0(0), qo, A);
+            const double Wt = unit_rates(P, 0, lane, sh, P.W0(0), qo, A);
             const double We = beta ? Wt : 0.0, Wo = beta ? 0.0 : Wt;
             const double Ne = beta ? 0.0 : nu0, No = beta ? nu0 : 0.0;
 #pragma unroll
@@ -360,7 +358,7 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
             const int bit = 1 << rb;
 #pragma unroll
             for (int r = 0; r < R; r++) q[r] = qo[r ^ bit];
-            const double Wt = unit_rates(P, u, nb, sh, P.W0(u), q, A);
+            const double Wt = unit_rates(P, u, lane, sh, P.W0(u), q, A);
             const double nuu = a.nu[u];
 #pragma unroll
             for (int r = 0; r < R; r++) {
@@ -380,7 +378,8 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
                 q[2 * kk] = v.x;
                 q[2 * kk + 1] = v.y;
             }
-            const double Wt = unit_rates(P, u, nb, sh, busy ? P.W0(u) : 0.0, q, A);
+            const double w0u = P.W0(u);   // warp-wide shuffle: outside the lane-dependent select
+            const double Wt = unit_rates(P, u, lane, sh, busy ? w0u : 0.0, q, A);
             const double wn = busy ? 0.0 : a.nu[u];
 #pragma unroll
             for (int r = 0; r < R; r++) {
@@ -399,7 +398,7 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
                 q[2 * kk + 1] = v.y;
             }
             if ((warp >> b) & 1) {
-                const double Wt = unit_rates(P, u, nb, sh, P.W0(u), q, A);
+                const double Wt = unit_rates(P, u, lane, sh, P.W0(u), q, A);
 #pragma unroll
                 for (int r = 0; r < R; r++) A[r] = fma(Wt, q[r], A[r]);
             } else {
@@ -423,7 +422,7 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
                 for (int kk = 0; kk < 4; kk++) pre[kk] = ldg2(src + (kk << 6));
             }
             if ((t >> h) & 1u) {
-                const double Wt = unit_rates(P, u, nb, sh, P.W0(u), q, A);
+                const double Wt = unit_rates(P, u, lane, sh, P.W0(u), q, A);
 #pragma unroll
                 for (int r = 0; r < R; r++) A[r] = fma(Wt, q[r], A[r]);
             } else {
@@ -444,7 +443,7 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
                 lam[r] = 0.0;
                 one[r] = 1.0;
             }
-            const double Bt = unit_rates(P, a.N, nb, sh, P.W0(a.N), one, lam);
+            const double Bt = unit_rates(P, a.N, lane, sh, P.W0(a.N), one, lam);
 #pragma unroll
             for (int r = 0; r < R; r++) lam[r] = a.Lam - (lam[r] + Bt);
         }
@@ -473,8 +472,8 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
                 val[1] = out;
             } else {
                 act[r] = (a.active >> n) & 1u;
-                const double p = (s_x[n] * A[r] + s_y[n] * D[r]) * __drcp_rn(den);
-                const double2 ok = __ldg(a.omkap + j);
+                const double p = (s_x[n] * A[r] + s_y[n] * D[r]) * rcp_nr(den);
+                const double2 ok = ldg_ef(a.omkap + j);
                 pnew[r] = p;
                 val[0] = act[r] ? p : 0.0;
                 val[1] = act[r] ? p * ok.x : 0.0;
@@ -638,9 +637,18 @@ __device__ int tile_program(const P3Args &a, uint32_t t, double *W0, PairAcc3 &P
         P.val[y + 1] = vx;
         P.rm[y + 1] = mx;
     }
-    int nrec = P.n;
-    for (int k = 0; k < P.n; k++)   // one header per group
-        if (P.rm[k] && (k == 0 || P.rm[k - 1] != P.rm[k] || (P.key[k - 1] & 63) != (P.key[k] & 63))) nrec++;
+    // records: per unit with data: a lane table (16 records) if it has lane-only pairs,
+    // then 17 records per group of equal rm
+    int nrec = 0;
+    for (int k = 0; k < P.n; k++) {
+        const int u = (int)(P.key[k] & 63);
+        const bool first_u = (k == 0 || (int)(P.key[k - 1] & 63) != u);
+        if (P.rm[k] == 0) {
+            if (first_u) nrec += 16;
+        } else if (first_u || P.rm[k - 1] != P.rm[k]) {
+            nrec += 17;
+        }
+    }
     return nrec;
 }
 
@@ -665,8 +673,7 @@ __global__ void k_prog_write3(P3Args a, const uint32_t *__restrict__ order, cons
     PairAcc3 P;
     double W0[HQ_MAXN + 1];
     const int NVU = 9;
-    uint32_t LW = 0;
-    for (int u = 2; u <= 6; u++) LW |= 1u << u;
+    const uint32_t LM = 0x7cu;   // lane units 2..6
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.ntiles;
          i += (uint64_t)gridDim.x * blockDim.x) {
         uint4 *out = prog + off16[i];
@@ -674,57 +681,65 @@ __global__ void k_prog_write3(P3Args a, const uint32_t *__restrict__ order, cons
         if (tile_program(a, t, W0, P) < 0) continue;
         uint32_t info[32];
         for (int q = 0; q < 32; q++) info[q] = 0u;
-        // emit records unit by unit
-        uint32_t pos = 0;   // record index after the header
+        uint4 *data = out + V3_HDR16;
+        uint32_t pos = 0;   // data records written
         int k = 0;
         while (k < P.n) {
             const int u = (int)(P.key[k] & 63);
-            uint32_t nl = 0, ng = 0;
+            const bool pseudo = (u == a.N);
+            const bool lane_unit = !pseudo && u >= 2 && u <= 6;
             const uint32_t start = pos;
-            while (k < P.n && (int)(P.key[k] & 63) == u) {
-                const uint32_t S = P.key[k] >> 6;
-                const bool pseudo = (u == a.N);
-                uint32_t St = S & LW;
-                if (!pseudo && ((LW >> u) & 1u)) St |= 1u << u;   // lane/warp unit: own busy condition
-                const double c = P.val[k];
-                const uint4 rec = make_uint4((uint32_t)__double_as_longlong(c),
-                                             (uint32_t)((unsigned long long)__double_as_longlong(c) >> 32), St, 0u);
-                if (P.rm[k] == 0) {
-                    out[V3_HDR16 + pos++] = rec;
-                    nl++;
-                    k++;
-                    continue;
+            uint32_t inf = 0u;
+            // condition of a pair for lane l: its lane units (and, for a lane unit, the unit
+            // itself) busy, i.e. (S_t & ~(l << 2)) == 0
+            auto St_of = [&](int kk) -> uint32_t {
+                uint32_t St = (P.key[kk] >> 6) & LM;
+                if (lane_unit) St |= 1u << u;
+                return St;
+            };
+            if (P.rm[k] == 0) {   // lane-only pairs -> per-lane table of W0 + pairs
+                const int k0 = k;
+                while (k < P.n && (int)(P.key[k] & 63) == u && P.rm[k] == 0) k++;
+                double *tab = reinterpret_cast<double *>(data + pos);
+                for (int l = 0; l < 32; l++) {
+                    const uint32_t busy = (uint32_t)l << 2;
+                    double w = (lane_unit && !((busy >> u) & 1u)) ? 0.0 : W0[u];
+                    for (int kk = k0; kk < k; kk++)
+                        if ((St_of(kk) & ~busy) == 0u) w += P.val[kk];
+                    tab[l] = w;
                 }
-                // group of equal rm: header then pairs
+                pos += 16;
+                inf |= 1u << 31;
+            }
+            uint32_t ng = 0;
+            while (k < P.n && (int)(P.key[k] & 63) == u) {   // groups of equal rm
                 const uint16_t rm = P.rm[k];
-                const uint32_t hpos = pos++;
-                uint32_t cnt = 0;
-                while (k < P.n && (int)(P.key[k] & 63) == u && P.rm[k] == rm) {
-                    const uint32_t S2 = P.key[k] >> 6;
-                    uint32_t St2 = S2 & LW;
-                    if (!pseudo && ((LW >> u) & 1u)) St2 |= 1u << u;
-                    const double c2 = P.val[k];
-                    out[V3_HDR16 + pos++] = make_uint4((uint32_t)__double_as_longlong(c2),
-                                                       (uint32_t)((unsigned long long)__double_as_longlong(c2) >> 32),
-                                                       St2, 0u);
-                    cnt++;
-                    k++;
+                const int k0 = k;
+                while (k < P.n && (int)(P.key[k] & 63) == u && P.rm[k] == rm) k++;
+                data[pos] = make_uint4((uint32_t)rm, 0u, 0u, 0u);
+                double *tab = reinterpret_cast<double *>(data + pos + 1);
+                for (int l = 0; l < 32; l++) {
+                    const uint32_t busy = (uint32_t)l << 2;
+                    double w = 0.0;
+                    for (int kk = k0; kk < k; kk++)
+                        if ((St_of(kk) & ~busy) == 0u) w += P.val[kk];
+                    tab[l] = w;
                 }
-                out[V3_HDR16 + hpos] = make_uint4(0u, 0u, cnt, (uint32_t)rm);
+                pos += 17;
                 ng++;
             }
-            if (nl > 255 || ng > 255) atomicExch(err, 3);
-            info[u] = nl | (ng << 8) | (start << 16);
+            if (ng > 255 || start > 0xffffu) atomicExch(err, 3);
+            info[u] = inf | ng | (start << 8);
         }
-        uint32_t has = 0;
-        for (int q = 0; q < 32; q++)
-            if (info[q]) has |= 1u << q;
         for (int q = 0; q < 8; q++) out[q] = make_uint4(info[4 * q], info[4 * q + 1], info[4 * q + 2], info[4 * q + 3]);
         double *w0o = reinterpret_cast<double *>(out + 8);
         for (int u = 0; u < 32; u++) w0o[u] = u <= HQ_MAXN ? W0[u] : 0.0;
         double muF = 0.0;
         for (int u = NVU; u < a.N; u++)
             if ((t >> (u - NVU)) & 1u) muF += a.nu[u];
+        uint32_t has = 0;
+        for (int q = 0; q < 32; q++)
+            if (info[q]) has |= 1u << q;
         out[24] = make_uint4((uint32_t)__double_as_longlong(muF),
                              (uint32_t)((unsigned long long)__double_as_longlong(muF) >> 32), has, 0u);
     }
@@ -747,7 +762,9 @@ size_t sweep_smem(int nW, uint32_t maxblk16, int nslots) {
     (void)nslots;
     const size_t TS = (size_t)1 << (8 + nW);
     // tile blocks, program blocks, per-warp flush scratch (32 lanes x 3 bins x 5 values)
-    return 2 * TS * 8 + 2 * (size_t)maxblk16 * 16 + ((size_t)1 << nW) * 32 * 3 * 5 * 8;
+    (void)maxblk16;
+    // double-buffered tile blocks + per-warp flush scratch (32 lanes x 3 bins)
+    return 2 * TS * 8 + ((size_t)1 << nW) * 32 * 3 * 8;
 }
 
 int choose_slots(int nW, uint32_t maxblk16) { return sweep_smem(nW, maxblk16, 0) <= 224u * 1024u ? 1 : 0; }
@@ -766,6 +783,10 @@ template <int MODE, bool FULL>
 static cudaError_t launch(const S3Args &a, int grid, cudaStream_t s) {
     const size_t sm = sweep_smem(a.nW, a.maxblk16, a.nslots);
     cudaError_t e = cudaFuncSetAttribute(hq3::k_sweep3<MODE, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    // leave the rest of the unified L1/shared array to L1 (rate programs are read through it)
+    const int carve = (int)std::min<size_t>(100, (sm + 2048) * 100 / (228 * 1024) + 1);
+    e = cudaFuncSetAttribute(hq3::k_sweep3<MODE, FULL>, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
     if (e != cudaSuccess) return e;
     hq3::k_sweep3<MODE, FULL><<<grid, 32 << a.nW, sm, s>>>(a);
     return cudaGetLastError();

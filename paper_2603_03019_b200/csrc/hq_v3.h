@@ -48,6 +48,7 @@ struct S3Args {
     const uint4 *prog;
     uint32_t total16;
     uint32_t maxblk16;       // largest program block of a CTA tile (16-byte units)
+    const uint32_t *range;   // [grid + 1]: CTA b processes visit indices [range[b], range[b+1])
     int nslots;              // CTA ring slots
     const double *Q;         // neighbour class (read)
     double *P;               // updated class (sweep) / evaluated class (residual)
