@@ -211,15 +211,16 @@ std::vector<int> choose_perm(int N, const TrieHost &tr) {
 }
 
 
-// Internal unit order for the CTA-tiled path (hq_v3.h): units 0 (parity),
-// 1, 7, 8 (register bits), 2..6 (lanes), 9..8+nW (warps) vary inside a tile;
-// the rest ("H") are fixed per tile.  Units that most often precede other
-// units in the preference lists become H (their nodes fold into the
-// tile-uniform rate part); among the varying units, the four register-class
-// slots go to the units whose choice minimises the expected cost of
-// register-dependent pairs (about 8x a lane-only pair) over random tiles.
+// Internal unit order for the CTA-tiled path (hq_v3.h).  Rate programs are per warp
+// tile: only units 0 (parity), 1, 7, 8 (register bits) and 2..6 (lanes) vary inside a
+// program; every other unit is fixed per program and its trie nodes fold into the
+// warp-tile-uniform rates.  So the nine units that least often precede other units in the
+// preference lists vary, and among them the four register-class slots (whose pairs need
+// per-state masks, the expensive "groups") go to the units that minimise the expected
+// number of register-dependent nodes alive in a random warp tile.  Warp and tile units
+// follow in order of increasing prefix count.
 std::vector<int> choose_perm_v3(int N, const TrieHost &tr, int nW) {
-    const int NVU = 9 + nW;
+    (void)nW;
     std::vector<int> perm(N);
     for (int u = 0; u < N; u++) perm[u] = u;
     const char *env = getenv("HQ_PERM");
@@ -239,30 +240,25 @@ std::vector<int> choose_perm_v3(int N, const TrieHost &tr, int nW) {
     std::vector<int> idx(N);
     for (int u = 0; u < N; u++) idx[u] = u;
     std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return cnt[a] < cnt[b]; });
-    std::vector<int> V(idx.begin(), idx.begin() + NVU);
+    std::vector<int> V(idx.begin(), idx.begin() + 9);
     uint32_t vmask = 0;
     for (int x : V) vmask |= 1u << x;
-    // node weight: probability that its tile-unit prefix is busy in a random tile
+    // node weight: probability that its fixed-unit path is busy in a random warp tile
     std::vector<double> w(tr.node.size());
     for (size_t v = 0; v < tr.node.size(); v++) {
         const int u = tr.node[v].x & 0xff;
-        const uint32_t path = pre[v] | (1u << u);
-        w[v] = std::ldexp(1.0, -__builtin_popcount(path & ~vmask));
+        w[v] = std::ldexp(1.0, -__builtin_popcount((pre[v] | (1u << u)) & ~vmask));
     }
     double best = 1e300;
     uint32_t bestT = 0;
-    const int nv = (int)V.size();
-    for (int a1 = 0; a1 < nv; a1++)
-        for (int a2 = a1 + 1; a2 < nv; a2++)
-            for (int a3 = a2 + 1; a3 < nv; a3++)
-                for (int a4 = a3 + 1; a4 < nv; a4++) {
+    for (int a1 = 0; a1 < 9; a1++)
+        for (int a2 = a1 + 1; a2 < 9; a2++)
+            for (int a3 = a2 + 1; a3 < 9; a3++)
+                for (int a4 = a3 + 1; a4 < 9; a4++) {
                     const uint32_t T = (1u << V[a1]) | (1u << V[a2]) | (1u << V[a3]) | (1u << V[a4]);
                     double cost = 0.0;
-                    for (size_t v = 0; v < tr.node.size(); v++) {
-                        const uint32_t S = pre[v] & vmask;
-                        if (!S) continue;
-                        cost += (S & T) ? 8.0 * w[v] : w[v];
-                    }
+                    for (size_t v = 0; v < tr.node.size(); v++)
+                        if (pre[v] & T) cost += w[v];
                     if (cost < best) {
                         best = cost;
                         bestT = T;
@@ -274,13 +270,10 @@ std::vector<int> choose_perm_v3(int N, const TrieHost &tr, int nW) {
     perm[1] = regc[1];
     perm[7] = regc[2];
     perm[8] = regc[3];
-    int k = 0;
-    for (int u = 2; u <= 6; u++) perm[u] = rest[k++];
-    for (int u = 9; u < NVU; u++) perm[u] = rest[k++];
-    for (int q = NVU; q < N; q++) perm[q] = idx[q];
+    for (int u = 2; u <= 6; u++) perm[u] = rest[u - 2];
+    for (int q = 9; q < N; q++) perm[q] = idx[q];
     return perm;
 }
-
 }  // namespace
 
 struct hq_problem {
@@ -709,7 +702,10 @@ static hq_status v2_prepare(hq_problem *h, cudaStream_t s) {
     cudaFree(tmp);
     cudaFree(tmp2);
     cudaFree(d_max);
-    if (h->path == 3) h->nslots = hq3_launch::choose_slots(h->nW, h->maxrec);
+    if (h->path == 3) {   // staged program capacity; larger blocks are read from global memory
+        h->maxrec = hq3_launch::choose_cap(h->nW, h->maxrec);
+        h->nslots = hq3_launch::choose_slots(h->nW, h->maxrec);
+    }
     if (h->path == 3 ? h->nslots < 1 : hq2_launch::sweep_smem(h->maxrec) > 150u * 1024u) {
         h->err = "rate program of a tile exceeds the shared-memory budget";
         return HQ_E_NUMERIC;

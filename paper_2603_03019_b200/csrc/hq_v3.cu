@@ -111,15 +111,63 @@ __device__ __forceinline__ void padd(double &W, const uint4 &x, uint32_t nb) {
         : "r"(x.x), "r"(x.y), "r"(x.z), "r"(nb));
 }
 
+// L2 cache policies (created once per thread)
+__device__ __forceinline__ uint64_t pol_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t pol_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+// 16-byte load of two adjacent states of the neighbour class (L1-allocating: the
+// slice was prefetched into L1 two units earlier), kept in L2 (every block is read by
+// the tiles of all its tile-unit neighbours)
+__device__ __forceinline__ double2 ldg2(const double *p, uint64_t pol) {
+    double2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+                 : "=d"(v.x), "=d"(v.y)
+                 : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ double2 ldg2p(const double2 *p, uint64_t pol) {
+    double2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+                 : "=d"(v.x), "=d"(v.y)
+                 : "l"(p), "l"(pol));
+    return v;
+}
+// bring a byte range into L2 ahead of use (bulk prefetch, no completion tracking)
+__device__ __forceinline__ void prefetch_l2(const void *p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void prefetch_l1(const void *p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+// rate-program reads: through L1, evicted first from L2 (read once per half-sweep)
+__device__ __forceinline__ double ldp(const double *p, uint64_t pol) {
+    double v;
+    asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ uint32_t ldpu(const uint32_t *p, uint64_t pol) {
+    uint32_t v;
+    asm volatile("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+}
+
 // Rate program of a warp tile (hq_v3.h): per unit either nothing (the warp-tile-uniform
-// rate W0[u] applies to every lane) or a data block with a per-lane table of the
-// thread-level rate (W0 plus the lane-conditioned pairs, summed at precompute time) and
-// groups of register-dependent pairs, each a mask of admissible register states and a
-// per-lane table of their summed rate.
+// rate W0[u] applies to every lane) or a data block: a table of the thread-level rate
+// (W0 plus the lane-conditioned pairs, summed at precompute time) over the lane bits M
+// its conditions use, then groups of register-dependent pairs, each a mask of admissible
+// register states and a table of their summed rate.  Entry of lane l: pext(l, M), looked
+// up in a 32 x 32 byte table.  The program block of a CTA tile is staged in shared memory
+// with the tile's q block (generic pointer: oversized blocks stay in global memory).
 struct Prog {
-    const uint4 *__restrict__ pg;   // header (global memory, read through L1)
-    uint32_t info;                  // info[lane] (broadcast to the unit being processed by shuffles)
-    double w0;                      // W0[lane]
+    const uint4 *pg;        // header
+    const uint8_t *pext;    // pext[M * 32 + lane]
+    uint32_t info;          // info[lane] (broadcast to the unit being processed by shuffles)
+    double w0;              // W0[lane]
     __device__ __forceinline__ double W0(int u) const { return __shfl_sync(0xffffffffu, w0, u); }
 };
 __device__ __forceinline__ double unit_rates(const Prog &P, int u, int lane, int sh, double w0,
@@ -129,14 +177,17 @@ __device__ __forceinline__ double unit_rates(const Prog &P, int u, int lane, int
     const uint4 *d = P.pg + V3_HDR16 + ((inf >> 8) & 0xffffu);
     double Wt = w0;
     if (inf >> 31) {
-        Wt = __ldg(reinterpret_cast<const double *>(d) + lane);
-        d += 16;
+        const uint32_t M = (inf >> 24) & 0x1fu;
+        Wt = reinterpret_cast<const double *>(d)[P.pext[M * 32 + lane]];
+        d += ((1 << __popc(M)) + 1) >> 1;
     }
     const int ng = (int)(inf & 0xffu);
     for (int g = 0; g < ng; g++) {
-        const uint32_t m8 = (__ldg(&d->x) >> sh) & 0xffu;
-        const double w = __ldg(reinterpret_cast<const double *>(d + 1) + lane);
-        d += 17;
+        const uint32_t hd = d->x;
+        const uint32_t M = (hd >> 16) & 0x1fu;
+        const uint32_t m8 = (hd >> sh) & 0xffu;
+        const double w = reinterpret_cast<const double *>(d + 1)[P.pext[M * 32 + lane]];
+        d += 1 + (((1 << __popc(M)) + 1) >> 1);
 #pragma unroll
         for (int r = 0; r < R; r++) pfma(A[r], w, q[r], m8 & (1u << r));
     }
@@ -173,12 +224,8 @@ __device__ __forceinline__ double2 ldg_ef(const double2 *p) {
     return v;
 }
 
-// coalesced read-only 16-byte load of two adjacent states, no L1 allocation
-__device__ __forceinline__ double2 ldg2(const double *p) {
-    double2 v;
-    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
-    return v;
-}
+
+
 
 template <int MODE, bool FULL>
 __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
@@ -187,13 +234,19 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t tbar[2];
     __shared__ double s_x[32], s_y[32], s_z[32], s_mr[R];
+    __shared__ uint8_t s_pext[32 * 32];
 
     const int nW = a.nW, T = 8 + nW, NVU = 9 + nW, nH = a.N - NVU;
     const int tid = threadIdx.x, lane = tid & 31, warp = wuni(tid >> 5);
     const unsigned nwarps = 1u << nW;
     const uint32_t TS = 1u << T;
-    double *tileq = reinterpret_cast<double *>(smem_raw);                    // [2][TS]
-    double *fscr = tileq + 2 * TS + (size_t)warp * 32 * 3;                  // per-warp flush scratch
+    // smem: tile buffers [2][q block TS doubles | program block maxblk16 records],
+    //       per-thread layer bins [3 * NB][threads], per-warp flush scratch [warps][32 * 3]
+    const size_t BUFD = TS + 2 * (size_t)a.maxblk16;
+    double *tileq = reinterpret_cast<double *>(smem_raw);
+    double *sb = tileq + 2 * BUFD;                                  // sb[(h * NB + v) * nthreads + tid]
+    const int nthr = 32 << nW;
+    double *fscr = sb + (size_t)3 * NB * nthr + (size_t)warp * 32 * 3;
 
     if (tid < 32) {
         if (MODE == 2) {
@@ -209,6 +262,13 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
         if (tid < R)
             s_mr[tid] = ((tid & 1) ? a.nu[1] : 0.0) + ((tid & 2) ? a.nu[7] : 0.0) + ((tid & 4) ? a.nu[8] : 0.0);
     }
+    for (int i = tid; i < 32 * 32; i += blockDim.x) {   // pext of lane bits: s_pext[M * 32 + l]
+        const uint32_t M = (uint32_t)i >> 5, l = (uint32_t)i & 31u;
+        uint32_t r = 0;
+        for (int b = 0, j = 0; b < 5; b++)
+            if ((M >> b) & 1u) r |= ((l >> b) & 1u) << j++;
+        s_pext[i] = (uint8_t)r;
+    }
     if (tid == 0) {
         mbar_init(sptr(&tbar[0]), 1);
         mbar_init(sptr(&tbar[1]), 1);
@@ -217,29 +277,27 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
     __syncthreads();
 
     // tiles of this CTA: a contiguous range of the popcount-sorted visit order, cut by the
-    // host so that every CTA gets the same estimated work (few layer flushes, no stragglers)
+    // host so that every CTA gets the same estimated work
     const uint32_t i0 = __ldg(a.range + blockIdx.x), i1 = __ldg(a.range + blockIdx.x + 1);
     const int nt = (int)(i1 - i0);
+    const uint64_t nwt = (uint64_t)a.ntiles << nW;
 
-    // ---- tile loader (thread 0): q block of the tile, double-buffered
+    // ---- tile loader (thread 0): q block + program block of tile k, double-buffered
     auto load_tile = [&](int k) {
-        const uint32_t t = __ldg(a.order + ((uint64_t)(i0 + k) << nW)) >> nW;
+        const uint64_t widx = (uint64_t)(i0 + k) << nW;
+        const uint32_t t = __ldg(a.order + widx) >> nW;
+        const uint32_t o = __ldg(a.off16 + widx);
+        const uint32_t nrec = (widx + nwarps < nwt ? __ldg(a.off16 + widx + nwarps) : a.total16) - o;
+        const bool staged = nrec <= a.maxblk16;
         const int buf = k & 1;
         const unsigned bar = sptr(&tbar[buf]);
-        mbar_expect(bar, TS * 8u);
-        bulk_g2s(sptr(tileq + (size_t)buf * TS), a.Q + ((size_t)t << T), TS * 8u, bar);
+        double *b = tileq + (size_t)buf * BUFD;
+        mbar_expect(bar, TS * 8u + (staged ? nrec * 16u : 0u));
+        bulk_g2s(sptr(b), a.Q + ((size_t)t << T), TS * 8u, bar);
+        if (staged) bulk_g2s(sptr(b + TS), a.prog + o, nrec * 16u, bar);
     };
-    // ---- program prefetch: this warp's program of tile k into L1
-    auto prefetch_prog = [&](int k) {
-        const uint64_t widx = ((uint64_t)(i0 + k) << nW) + warp;
-        const uint32_t o = __ldg(a.off16 + widx);
-        const uint32_t e = widx + 1 < ((uint64_t)a.ntiles << nW) ? __ldg(a.off16 + widx + 1) : a.total16;
-        const char *b = reinterpret_cast<const char *>(a.prog + o);
-        const uint32_t nl = ((e - o) * 16u + 127u) / 128u + 1u;
-        for (uint32_t x = lane; x < nl; x += 32) asm volatile("prefetch.global.L1 [%0];" ::"l"(b + 128 * (size_t)x));
-    };
+
     if (tid == 0 && nt > 0) load_tile(0);
-    if (nt > 0) prefetch_prog(0);
 
     // ---- per-thread constants
     double mu_t = 0.0;
@@ -250,20 +308,19 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
     const int par_t = popc_t & 1;
     const uint32_t jw = ((uint32_t)warp << 8) | ((uint32_t)lane << 1);   // j_local(r) = jw | (r>>1)<<6 | (r&1)
     const double nu0 = a.nu[0];
+    const uint64_t pol_ef = pol_evict_first(), pol_el = pol_evict_last();
 
     double acc[NB];   // lane L: layer L
 #pragma unroll
     for (int v = 0; v < NB; v++) acc[v] = 0.0;
-    double bins[3][NB];
+    // per-thread layer bins (bin h of this thread = layer K + popc_t + beta + 2h), in smem
 #pragma unroll
     for (int h = 0; h < 3; h++)
 #pragma unroll
-        for (int v = 0; v < NB; v++) bins[h][v] = 0.0;
+        for (int v = 0; v < NB; v++) sb[(h * NB + v) * nthr + tid] = 0.0;
     int curK = -1;
 
     // layer of bin h of this thread at tile popcount K: K + popc_t + beta + 2h.
-    // Flush: lanes write their bins to a per-warp scratch; lane y (< 6 NB) sums, in
-    // lane order, the entries that fall on relative layer y / NB of the warp.
     auto flush = [&]() {
         if (curK < 0) return;
         const int betaK = a.c ^ (curK & 1) ^ par_t;
@@ -274,7 +331,7 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
 #pragma unroll
         for (int v = 0; v < NB; v++) {
 #pragma unroll
-            for (int h = 0; h < 3; h++) fscr[lane * 3 + h] = bins[h][v];
+            for (int h = 0; h < 3; h++) fscr[lane * 3 + h] = sb[(h * NB + v) * nthr + tid];
             __syncwarp();
             double s = 0.0;
             for (int l = 0; l < 32; l++) {   // fixed lane order
@@ -291,33 +348,41 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
 #pragma unroll
         for (int h = 0; h < 3; h++)
 #pragma unroll
-            for (int v = 0; v < NB; v++) bins[h][v] = 0.0;
+            for (int v = 0; v < NB; v++) sb[(h * NB + v) * nthr + tid] = 0.0;
     };
 
     for (int k = 0; k < nt; k++) {
         const uint64_t widx = (uint64_t)(i0 + k) << nW;
-        const uint32_t t = (uint32_t)wuni((int)(__ldg(a.order + widx) >> nW));
+        const uint32_t t = __ldg(a.order + widx) >> nW;
         const uint32_t jt = t << T;
         const int buf = k & 1;
-        // first tile-unit neighbours: in flight while the tile block arrives
-        double2 pre[4];
+        // tile-unit neighbour slices: two units of loads in flight ahead of the one accumulated
+        auto hsrc = [&](int h) -> const double * { return a.Q + ((jt ^ (1u << (T + h))) | jw); };
+        double2 pa[4], pb2[4];
         if (nH > 0) {
-            const double *src = a.Q + ((jt ^ (1u << T)) | jw);
 #pragma unroll
-            for (int kk = 0; kk < 4; kk++) pre[kk] = ldg2(src + (kk << 6));
+            for (int kk = 0; kk < 4; kk++) pa[kk] = ldg2(hsrc(0) + (kk << 6), pol_el);
+        }
+        if (nH > 1) {
+#pragma unroll
+            for (int kk = 0; kk < 4; kk++) pb2[kk] = ldg2(hsrc(1) + (kk << 6), pol_el);
         }
         mbar_wait(sptr(&tbar[buf]), (unsigned)((k >> 1) & 1));
-        __syncthreads();   // every warp is done with tile k-1: its buffers may be refilled
+        __syncthreads();   // every warp is done with tile k-1: its buffer may be refilled
         if (tid == 0 && k + 1 < nt) {
             fence_proxy_async();
             load_tile(k + 1);
         }
-        if (k + 1 < nt) prefetch_prog(k + 1);
-        const double *tq = tileq + (size_t)buf * TS;
+        const double *tq = tileq + (size_t)buf * BUFD;
         Prog P;
-        P.pg = a.prog + __ldg(a.off16 + widx + warp);
-        P.info = __ldg(reinterpret_cast<const uint32_t *>(P.pg) + lane);
-        P.w0 = __ldg(reinterpret_cast<const double *>(P.pg + 8) + lane);
+        {
+            const uint32_t o0 = __ldg(a.off16 + widx), ow = __ldg(a.off16 + widx + warp);
+            const uint32_t nrec = (widx + nwarps < nwt ? __ldg(a.off16 + widx + nwarps) : a.total16) - o0;
+            P.pg = nrec <= a.maxblk16 ? reinterpret_cast<const uint4 *>(tq + TS) + (ow - o0) : a.prog + ow;
+            P.pext = s_pext;
+            P.info = reinterpret_cast<const uint32_t *>(P.pg)[lane];
+            P.w0 = reinterpret_cast<const double *>(P.pg + 8)[lane];
+        }
         const int K = __popc(t);
         if (K != curK) {
             flush();
@@ -325,7 +390,7 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
         }
         const int beta = a.c ^ (K & 1) ^ par_t;
         const int sh = beta ? 8 : 0;
-        const double mu_F = __ldg(reinterpret_cast<const double *>(P.pg + 24));
+        const double mu_F = reinterpret_cast<const double *>(P.pg + 24)[0];
 
         double qo[R], A[R], D[R], q[R];
 #pragma unroll
@@ -366,7 +431,7 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
                 else D[r] = fma(nuu, q[r], D[r]);
             }
         }
-        // ---- lane units 2..6 (lane bits 0..4): busy per lane; their pairs carry the own bit
+        // ---- lane units 2..6 (lane bits 0..4): busy per lane
 #pragma unroll
         for (int b = 0; b < 5; b++) {
             const int u = 2 + b;
@@ -407,19 +472,19 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
                 for (int r = 0; r < R; r++) D[r] = fma(nuu, q[r], D[r]);
             }
         }
-        // ---- tile units (H): neighbour tile slices straight from global memory (L2),
-        //      one unit of loads in flight ahead of the unit being accumulated
+        // ---- tile units (H): neighbour tile slices straight from global memory (L2)
         for (int h = 0; h < nH; h++) {
             const int u = NVU + h;
 #pragma unroll
             for (int kk = 0; kk < 4; kk++) {
-                q[2 * kk] = pre[kk].x;
-                q[2 * kk + 1] = pre[kk].y;
+                q[2 * kk] = pa[kk].x;
+                q[2 * kk + 1] = pa[kk].y;
+                pa[kk] = pb2[kk];
             }
-            if (h + 1 < nH) {
-                const double *src = a.Q + ((jt ^ (1u << (T + h + 1))) | jw);
+            if (h + 2 < nH) {
+                const double *src = hsrc(h + 2);
 #pragma unroll
-                for (int kk = 0; kk < 4; kk++) pre[kk] = ldg2(src + (kk << 6));
+                for (int kk = 0; kk < 4; kk++) pb2[kk] = ldg2(src + (kk << 6), pol_el);
             }
             if ((t >> h) & 1u) {
                 const double Wt = unit_rates(P, u, lane, sh, P.W0(u), q, A);
@@ -447,11 +512,16 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
 #pragma unroll
             for (int r = 0; r < R; r++) lam[r] = a.Lam - (lam[r] + Bt);
         }
-        // ---- epilogue (own old p and scatter weights straight from global memory)
+        // ---- epilogue
         const int base = K + popc_t;
         const double mu_base = mu_F + mu_t;
         double pnew[R];
         bool act[R];
+        double bins[3][NB];
+#pragma unroll
+        for (int h = 0; h < 3; h++)
+#pragma unroll
+            for (int v = 0; v < NB; v++) bins[h][v] = 0.0;
 #pragma unroll
         for (int r = 0; r < R; r++) {
             const int pc = __popc(r);
@@ -473,7 +543,7 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
             } else {
                 act[r] = (a.active >> n) & 1u;
                 const double p = (s_x[n] * A[r] + s_y[n] * D[r]) * rcp_nr(den);
-                const double2 ok = ldg_ef(a.omkap + j);
+                const double2 ok = ldg2p(a.omkap + j, pol_ef);
                 pnew[r] = p;
                 val[0] = act[r] ? p : 0.0;
                 val[1] = act[r] ? p * ok.x : 0.0;
@@ -496,6 +566,10 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
                 }
             }
         }
+#pragma unroll
+        for (int h = 0; h < 3; h++)
+#pragma unroll
+            for (int v = 0; v < NB; v++) sb[(h * NB + v) * nthr + tid] += bins[h][v];
         if (MODE < 2) {
 #pragma unroll
             for (int kk = 0; kk < 4; kk++) {
@@ -511,7 +585,7 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
     }
     flush();
     // ---- CTA partials: warp w's lane L holds layer L; fixed-order sum over warps
-    __syncthreads();   // no copy in flight: reuse the tile buffers
+    __syncthreads();   // every copy consumed: reuse the tile buffers
     double *red = tileq;
 #pragma unroll
     for (int v = 0; v < NB; v++) red[((size_t)warp * 32 + lane) * NB + v] = acc[v];
@@ -637,17 +711,20 @@ __device__ int tile_program(const P3Args &a, uint32_t t, double *W0, PairAcc3 &P
         P.val[y + 1] = vx;
         P.rm[y + 1] = mx;
     }
-    // records: per unit with data: a lane table (16 records) if it has lane-only pairs,
-    // then 17 records per group of equal rm
+    // records: per unit with data: a lane table if it has lane-only pairs, then one group
+    // per distinct rm; a table over the lane bits M its conditions use has 2^|M| entries
+    // (ceil(2^|M| / 2) records); a group adds one header record
     int nrec = 0;
-    for (int k = 0; k < P.n; k++) {
+    int k = 0;
+    while (k < P.n) {
         const int u = (int)(P.key[k] & 63);
-        const bool first_u = (k == 0 || (int)(P.key[k - 1] & 63) != u);
-        if (P.rm[k] == 0) {
-            if (first_u) nrec += 16;
-        } else if (first_u || P.rm[k - 1] != P.rm[k]) {
-            nrec += 17;
+        const uint16_t rm = P.rm[k];
+        uint32_t M = (!(u == a.N) && u >= 2 && u <= 6) ? (1u << (u - 2)) : 0u;
+        while (k < P.n && (int)(P.key[k] & 63) == u && P.rm[k] == rm) {
+            M |= (P.key[k] >> 8) & 0x1fu;   // lane units 2..6 of S -> lane bits 0..4
+            k++;
         }
+        nrec += (rm ? 1 : 0) + (((1 << __popc(M)) + 1) >> 1);
     }
     return nrec;
 }
@@ -668,12 +745,18 @@ __global__ void k_prog_count3(P3Args a, const uint32_t *__restrict__ order, uint
     }
 }
 
+__device__ __forceinline__ uint32_t pdep5(uint32_t idx, uint32_t M) {   // deposit idx bits into the set bits of M
+    uint32_t r = 0;
+    for (int b = 0, i = 0; b < 5; b++)
+        if ((M >> b) & 1u) r |= ((idx >> i++) & 1u) << b;
+    return r;
+}
+
 __global__ void k_prog_write3(P3Args a, const uint32_t *__restrict__ order, const uint32_t *__restrict__ off16,
                               uint4 *__restrict__ prog, int *__restrict__ err) {
     PairAcc3 P;
     double W0[HQ_MAXN + 1];
     const int NVU = 9;
-    const uint32_t LM = 0x7cu;   // lane units 2..6
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.ntiles;
          i += (uint64_t)gridDim.x * blockDim.x) {
         uint4 *out = prog + off16[i];
@@ -686,47 +769,45 @@ __global__ void k_prog_write3(P3Args a, const uint32_t *__restrict__ order, cons
         int k = 0;
         while (k < P.n) {
             const int u = (int)(P.key[k] & 63);
-            const bool pseudo = (u == a.N);
-            const bool lane_unit = !pseudo && u >= 2 && u <= 6;
+            const bool lane_unit = (u != a.N) && u >= 2 && u <= 6;
             const uint32_t start = pos;
-            uint32_t inf = 0u;
-            // condition of a pair for lane l: its lane units (and, for a lane unit, the unit
-            // itself) busy, i.e. (S_t & ~(l << 2)) == 0
-            auto St_of = [&](int kk) -> uint32_t {
-                uint32_t St = (P.key[kk] >> 6) & LM;
-                if (lane_unit) St |= 1u << u;
-                return St;
-            };
-            if (P.rm[k] == 0) {   // lane-only pairs -> per-lane table of W0 + pairs
-                const int k0 = k;
-                while (k < P.n && (int)(P.key[k] & 63) == u && P.rm[k] == 0) k++;
-                double *tab = reinterpret_cast<double *>(data + pos);
-                for (int l = 0; l < 32; l++) {
-                    const uint32_t busy = (uint32_t)l << 2;
-                    double w = (lane_unit && !((busy >> u) & 1u)) ? 0.0 : W0[u];
-                    for (int kk = k0; kk < k; kk++)
-                        if ((St_of(kk) & ~busy) == 0u) w += P.val[kk];
-                    tab[l] = w;
-                }
-                pos += 16;
-                inf |= 1u << 31;
-            }
-            uint32_t ng = 0;
-            while (k < P.n && (int)(P.key[k] & 63) == u) {   // groups of equal rm
+            uint32_t inf = 0u, ng = 0u;
+            while (k < P.n && (int)(P.key[k] & 63) == u) {
                 const uint16_t rm = P.rm[k];
                 const int k0 = k;
-                while (k < P.n && (int)(P.key[k] & 63) == u && P.rm[k] == rm) k++;
-                data[pos] = make_uint4((uint32_t)rm, 0u, 0u, 0u);
-                double *tab = reinterpret_cast<double *>(data + pos + 1);
-                for (int l = 0; l < 32; l++) {
-                    const uint32_t busy = (uint32_t)l << 2;
-                    double w = 0.0;
-                    for (int kk = k0; kk < k; kk++)
-                        if ((St_of(kk) & ~busy) == 0u) w += P.val[kk];
-                    tab[l] = w;
+                uint32_t M = lane_unit ? (1u << (u - 2)) : 0u;
+                while (k < P.n && (int)(P.key[k] & 63) == u && P.rm[k] == rm) {
+                    M |= (P.key[k] >> 8) & 0x1fu;
+                    k++;
                 }
-                pos += 17;
-                ng++;
+                // table over the lane bits M: entry idx holds the value of every lane whose
+                // M-bits are pdep(idx, M); a pair applies when its lane units (and, for a
+                // lane unit, the unit itself) are busy in the lane
+                double *tab;
+                if (rm) {
+                    data[pos] = make_uint4((uint32_t)rm | (M << 16), 0u, 0u, 0u);
+                    tab = reinterpret_cast<double *>(data + pos + 1);
+                    pos += 1;
+                    ng++;
+                } else {
+                    tab = reinterpret_cast<double *>(data + pos);
+                    inf |= (1u << 31) | (M << 24);
+                }
+                const int ne = 1 << __popc(M);
+                for (int idx = 0; idx < ne; idx++) {
+                    const uint32_t lanebits = pdep5((uint32_t)idx, M);
+                    const uint32_t busy = lanebits << 2;
+                    double w = 0.0;
+                    if (!rm) w = (lane_unit && !((busy >> u) & 1u)) ? 0.0 : W0[u];
+                    for (int kk = k0; kk < k; kk++) {
+                        uint32_t St = (P.key[kk] >> 6) & 0x7cu;
+                        if (lane_unit) St |= 1u << u;
+                        if ((St & ~busy) == 0u) w += P.val[kk];
+                    }
+                    tab[idx] = w;
+                }
+                if (ne & 1) tab[ne] = 0.0;
+                pos += (uint32_t)((ne + 1) >> 1);
             }
             if (ng > 255 || start > 0xffffu) atomicExch(err, 3);
             info[u] = inf | ng | (start << 8);
@@ -760,13 +841,20 @@ int choose_nw(int N) {
 
 size_t sweep_smem(int nW, uint32_t maxblk16, int nslots) {
     (void)nslots;
-    const size_t TS = (size_t)1 << (8 + nW);
-    // tile blocks, program blocks, per-warp flush scratch (32 lanes x 3 bins x 5 values)
-    (void)maxblk16;
-    // double-buffered tile blocks + per-warp flush scratch (32 lanes x 3 bins)
-    return 2 * TS * 8 + ((size_t)1 << nW) * 32 * 3 * 8;
+    const size_t TS = (size_t)1 << (8 + nW), W = (size_t)1 << nW;
+    // tile buffers (q block + program block) x 2, per-thread layer bins (3 x 5 values),
+    // per-warp flush scratch
+    return 2 * (TS * 8 + (size_t)maxblk16 * 16) + W * 32 * 3 * 5 * 8 + W * 32 * 3 * 8;
 }
 
+// staged program capacity (records per tile block): as large as fits, at most the largest block
+uint32_t choose_cap(int nW, uint32_t maxblk16) {
+    const size_t budget = 224u * 1024u - 2048u;
+    const size_t fixed = sweep_smem(nW, 0, 0);
+    if (fixed >= budget) return 0;
+    const size_t cap = (budget - fixed) / (2 * 16);
+    return (uint32_t)std::min<size_t>(cap, maxblk16);
+}
 int choose_slots(int nW, uint32_t maxblk16) { return sweep_smem(nW, maxblk16, 0) <= 224u * 1024u ? 1 : 0; }
 
 cudaError_t prog_count(const P3Args &a, const uint32_t *order, uint32_t *size16, int *err, int grid, cudaStream_t s) {

@@ -75,5 +75,6 @@ cudaError_t prog_write(const P3Args &a, const uint32_t *order, const uint32_t *o
 cudaError_t sweep(const S3Args &a, int full, int mode, int grid, cudaStream_t s);
 size_t sweep_smem(int nW, uint32_t maxblk16, int nslots);
 int choose_slots(int nW, uint32_t maxblk16);
+uint32_t choose_cap(int nW, uint32_t maxblk16);
 int choose_nw(int N);
 }  // namespace hq3_launch

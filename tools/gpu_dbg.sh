@@ -1,2 +1,4 @@
-timeout 120 python tools/check_programs.py 12 40 0 4 > gpurun_out/chk12.log 2>&1; echo rc=$?; tail -12 gpurun_out/chk12.log
-timeout 120 python tools/check_programs.py 13 40 5 4 > gpurun_out/chk13.log 2>&1; echo rc=$?; tail -12 gpurun_out/chk13.log
+for cfg in 1 2 3; do
+  timeout 60 python tools/prof_solve.py $cfg 3 > gpurun_out/dbg_cfg$cfg.log 2>&1; echo "cfg$cfg rc=$?"; tail -c 300 gpurun_out/dbg_cfg$cfg.log; echo
+done
+timeout 200 python -m pytest tests/test_gpu_parity.py -m gpu -x -q --timeout 60 > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?; tail -3 gpurun_out/pytest_gpu.log
