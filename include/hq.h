@@ -132,7 +132,9 @@ const char *hq_error_string(hq_handle h);
  *   [8] time in the sweep kernels in ms (CUDA events), [9] sweep-kernel
  *   launches, [10] residual-kernel time in ms, [11] one-off per-instance
  *   precompute time in ms (rate programs, scatter weights), [12] bytes of
- *   rate programs, [13] code path (1: N < 8 two-pass, 2: tiled single pass).
+ *   rate programs, [13] code path (1: N < 8 two-pass, 2: warp-tiled, 3: CTA-tiled),
+ *   [14] largest rate-program block of a CTA tile (16-byte records),
+ *   [15] staged program capacity (records; larger blocks are read from global memory).
  */
 #define HQ_STATS_LEN 16
 hq_status hq_stats(hq_handle h, double *out);

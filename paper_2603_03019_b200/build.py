@@ -26,13 +26,16 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if force or _stale():
+def build(force: bool = False, verbose: bool = False, out: str = None, defines=()) -> str:
+    """Compile libhq.so (or a variant at `out` with extra -D defines, for A/B runs)."""
+    lib = out or LIB
+    if force or out or _stale():
         nvcc = os.environ.get("NVCC", "nvcc")
         extra = ["-DHQ_DEBUG_HANG"] if os.environ.get("HQ_DEBUG_HANG") else []
-        cmd = [nvcc] + NVCC_FLAGS + extra + (["-Xptxas", "-v"] if verbose else []) + ["-o", LIB] + SOURCES
+        extra += ["-D" + d for d in defines]
+        cmd = [nvcc] + NVCC_FLAGS + extra + (["-Xptxas", "-v"] if verbose else []) + ["-o", lib] + SOURCES
         subprocess.run(cmd, check=True)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

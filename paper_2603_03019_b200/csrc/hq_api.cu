@@ -307,6 +307,8 @@ struct hq_problem {
     int path = 1;                  // 1: N < 8 two-pass, 2: warp-tiled (hq_v2.cu), 3: CTA-tiled (hq_v3.cu)
     int nW = 0;                    // path 3: log2(warps per CTA)
     int nslots = 0;                // path 3: CTA ring slots
+    uint32_t maxblk_all = 0;       // path 3: largest program block of a CTA tile (records)
+    unsigned *d_done = nullptr;    // path 3: CTA completion counter of the fused scalar step
     uint32_t *d_order = nullptr, *d_off16 = nullptr, *d_size16 = nullptr, *d_range = nullptr;
     uint4 *d_prog = nullptr;
     double2 *d_omkap = nullptr;
@@ -344,6 +346,8 @@ struct hq_problem {
         cudaFree(d_order);
         cudaFree(d_range);
         d_range = nullptr;
+        cudaFree(d_done);
+        d_done = nullptr;
         cudaFree(d_off16);
         cudaFree(d_size16);
         cudaFree(d_prog);
@@ -697,12 +701,17 @@ static hq_status v2_prepare(hq_problem *h, cudaStream_t s) {
         cudaFree(h->d_range);
         h->d_range = nullptr;
         HQ_CUDA(cudaMalloc((void **)&h->d_range, 4 * (G + 1)));
+        if (!h->d_done) {
+            HQ_CUDA(cudaMalloc((void **)&h->d_done, sizeof(unsigned)));
+            HQ_CUDA(cudaMemset(h->d_done, 0, sizeof(unsigned)));
+        }
         HQ_CUDA(cudaMemcpy(h->d_range, range.data(), 4 * (G + 1), cudaMemcpyHostToDevice));
     }
     cudaFree(tmp);
     cudaFree(tmp2);
     cudaFree(d_max);
     if (h->path == 3) {   // staged program capacity; larger blocks are read from global memory
+        h->maxblk_all = h->maxrec;
         h->maxrec = hq3_launch::choose_cap(h->nW, h->maxrec);
         h->nslots = hq3_launch::choose_slots(h->nW, h->maxrec);
     }
@@ -764,6 +773,9 @@ static cudaError_t tiled_sweep(hq_problem *h, const S2Args &sa, int mode, cudaSt
     a.maxblk16 = sa.maxrec;
     a.nslots = h->nslots;
     a.range = h->d_range;
+    a.blk = h->d_blk;
+    a.done = h->d_done;
+    a.full_lists = sa.full_lists;
     a.Q = sa.Q;
     a.P = sa.P;
     a.omkap = sa.omkap;
@@ -864,8 +876,12 @@ static hq_status solve_v2(hq_problem *h, double tol, int max_iter, double *pi, c
         HQ_CUDA(cudaEventRecord(h->event(2 * (size_t)o.halfsweeps), s));
         HQ_CUDA(tiled_sweep(h, sa, checking ? 1 : 0, s));
         HQ_CUDA(cudaEventRecord(h->event(2 * (size_t)o.halfsweeps + 1), s));
-        HQ_CUDA(hq2_launch::scalars(N, sa.full_lists, h->Lam, 1, c, active, h->sgrid, h->d_partial, h->d_blk, s));
-        o.launches += 2;
+        if (h->path != 3 || !hq3_launch::fused_scalars()) {   // path 3: scalar step in the sweep's last CTA
+            HQ_CUDA(hq2_launch::scalars(N, sa.full_lists, h->Lam, 1, c, active, h->sgrid, h->d_partial, h->d_blk, s,
+                                        h->path == 3 ? 1 : 0));
+            o.launches++;
+        }
+        o.launches++;
         o.halfsweeps++;
         for (int n = 1; n <= N - 1; n++)
             if ((active >> n) & 1u) o.updates += binom(N, n);
@@ -974,6 +990,8 @@ extern "C" hq_status hq_solve(hq_handle h, double tol, int max_iter, double *pi,
         h->stats[11] = h->precompute_ms;
         h->stats[12] = h->prog_bytes;
         h->stats[13] = h->path;   // path id
+        h->stats[14] = h->maxblk_all;
+        h->stats[15] = h->maxrec;
         if (iters_out) *iters_out = o.sweeps;
         if (residual_out) *residual_out = o.res;
         if (!std::isfinite(o.res)) {

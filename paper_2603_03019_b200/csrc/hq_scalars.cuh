@@ -1,0 +1,104 @@
+// hq_scalars.cuh -- the per-layer scalar step shared by k_scalars2 (hq_v2.cu) and the
+// fused tail of the sweep kernel (hq_v3.cu).  Product code only.
+//
+// Given the per-layer sums S[n][v] of one half-sweep (v: V2_P, V2_OM, V2_KA, V2_LAM,
+// V2_DL1) or of the init / residual passes, update the scalar block `sb` (a shared-memory
+// copy of the V2S_* block):
+//   lambda(n) (Eq. lambdaHeter), mu(n) (Eq. muHeter via the exact flow
+//   identity sum_m p den = mu* + lambda_old(n)), the a-priori
+//   normalisers alpha(n) = mu*(n)/lambda(n-1) and beta(n) = lambda(n)/mu(n+1) of the next
+//   half-sweep, and p(n) by Eq. bnd_stationary.
+// Called by every thread of the block (contains __syncthreads); layers are processed in
+// parallel, the prefix product of Eq. bnd_stationary and the proxy sum by thread 0, so the
+// result does not depend on the block size.
+#pragma once
+#include "hq_internal.h"
+#include "hq_v2.h"
+
+__device__ __forceinline__ void scalars_update(int N, int full_lists, double Lam, int mode, int c, uint32_t active,
+                                               const double (*S)[NV2], double *sb) {
+    double *lam = sb + V2S_LAM, *mu = sb + V2S_MU, *al = sb + V2S_ALPHA, *be = sb + V2S_BETA;
+    double *pn1 = sb + V2S_PN, *om = sb + V2S_OM, *ka = sb + V2S_KA, *misc = sb + V2S_MISC;
+    const int tid = threadIdx.x;
+    __shared__ double s_g[HQ_NL];
+    __shared__ double s_tot;
+    __shared__ int s_err;
+    if (tid == 0) s_err = 0;
+    if (mode == 2) {
+        if (tid == 0) {
+            double num = 0.0, den = 0.0;
+            for (int L = 0; L <= N; L++) {
+                sb[V2S_RNUM + L] = S[L][V2_RNUM];
+                sb[V2S_RDEN + L] = S[L][V2_RDEN];
+                num += S[L][V2_RNUM];
+                den += S[L][V2_RDEN];
+            }
+            misc[1] = num / den;
+        }
+        __syncthreads();
+        return;
+    }
+    __syncthreads();
+    if (mode == 0) {
+        // init: S = {sum p, sum p mu_m, sum p omega, sum p kappa, sum p lambda_m} over both classes
+        for (int L = tid; L <= N; L += blockDim.x) {
+            lam[L] = S[L][4];
+            mu[L] = S[L][1];
+            om[L] = S[L][2];
+            ka[L] = S[L][3];
+            sb[V2S_SUMP + L] = S[L][0];
+            sb[V2S_DL1 + L] = 0.0;
+        }
+        c = 0;   // the first half-sweep updates class 1
+    } else {
+        // layers of one parity: lambda(L-1) of the other parity is read, never written here
+        for (int L = 1 + tid; L <= N - 1; L += blockDim.x) {
+            if (!((active >> L) & 1u)) continue;
+            const double lnew = full_lists ? Lam * S[L][V2_P] : S[L][V2_LAM];
+            const double mstar = al[L] * lam[L - 1];
+            const double mnew = mstar + lam[L] - lnew;
+            sb[V2S_MUSTAR + L] = mstar;
+            lam[L] = lnew;
+            mu[L] = mnew;
+            om[L] = S[L][V2_OM];
+            ka[L] = S[L][V2_KA];
+            sb[V2S_SUMP + L] = S[L][V2_P];
+            sb[V2S_DL1 + L] = S[L][V2_DL1];
+            if (!(S[L][V2_P] > 0.0) || !isfinite(mnew)) s_err = 1;
+        }
+    }
+    __syncthreads();
+    // coefficients for the next half-sweep (class 1 - c)
+    const int nc = 1 - c;
+    for (int L = 1 + tid; L <= N - 1; L += blockDim.x) {
+        if ((L & 1) != nc) continue;
+        const double b = lam[L] / mu[L + 1];
+        const double a = (1.0 - b * ka[L + 1]) / om[L - 1];
+        be[L] = b;
+        al[L] = a;
+        if (!(om[L - 1] > 0.0) || !isfinite(a) || !(a > 0.0)) s_err = 1;
+    }
+    // Eq. bnd_stationary: ratios in parallel, prefix product by thread 0
+    for (int L = 1 + tid; L <= N; L += blockDim.x) s_g[L] = lam[L - 1] / mu[L];
+    __syncthreads();
+    if (tid == 0) {
+        double prod = 1.0, tot = 1.0;
+        s_g[0] = 1.0;
+        for (int L = 1; L <= N; L++) {
+            prod *= s_g[L];
+            s_g[L] = prod;
+            tot += prod;
+        }
+        s_tot = tot;
+    }
+    __syncthreads();
+    for (int L = tid; L < 34; L += blockDim.x) pn1[L] = (L >= 1 && L <= N + 1) ? s_g[L - 1] / s_tot : 0.0;
+    __syncthreads();
+    if (tid == 0) {
+        double prox = 0.0;
+        for (int L = 1; L <= N - 1; L++) prox += pn1[L + 1] * sb[V2S_DL1 + L];
+        misc[2] = prox;
+        if (s_err) misc[0] = 1.0;
+    }
+    __syncthreads();
+}

@@ -31,6 +31,7 @@
 #include <cstdint>
 #include "hq_internal.h"
 #include "hq_v2.h"
+#include "hq_scalars.cuh"
 
 namespace hq2 {
 
@@ -662,10 +663,19 @@ __global__ void __launch_bounds__(WARPS * 32, 2) k_sweep2(S2Args a) {
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(1024) k_scalars2(int N, int full_lists, double Lam, int mode, int c, uint32_t active,
                                                     int ncta, const double *__restrict__ partial,
-                                                    double *__restrict__ blk) {
+                                                    double *__restrict__ blk, int transposed) {
     __shared__ double S[HQ_NL][NV2];
     const int lane = threadIdx.x & 31, n = threadIdx.x >> 5;
-    if (n <= N) {
+    if (transposed) {   // partial[(layer * HQ_NV + v) * ncta + cta]: one warp per (layer, value), coalesced
+        for (int i = n; i < HQ_NL * NV2; i += (int)(blockDim.x >> 5)) {
+            const int L = i / NV2, v = i - L * NV2;
+            const double *src = partial + ((size_t)L * HQ_NV + v) * ncta;
+            double s = 0.0;
+            for (int b = lane; b < ncta; b += 32) s += src[b];
+            s = warp_sum(s);
+            if (lane == 0) S[L][v] = s;
+        }
+    } else if (n <= N) {
         double s[NV2];
 #pragma unroll
         for (int v = 0; v < NV2; v++) s[v] = 0.0;
@@ -679,73 +689,12 @@ __global__ void __launch_bounds__(1024) k_scalars2(int N, int full_lists, double
         }
     }
     __syncthreads();
-    if (threadIdx.x != 0) return;
-    double *lam = blk + V2S_LAM, *mu = blk + V2S_MU, *al = blk + V2S_ALPHA, *be = blk + V2S_BETA;
-    double *pn1 = blk + V2S_PN, *om = blk + V2S_OM, *ka = blk + V2S_KA, *misc = blk + V2S_MISC;
-    if (mode == 2) {
-        double num = 0.0, den = 0.0;
-        for (int L = 0; L <= N; L++) {
-            blk[V2S_RNUM + L] = S[L][V2_RNUM];
-            blk[V2S_RDEN + L] = S[L][V2_RDEN];
-            num += S[L][V2_RNUM];
-            den += S[L][V2_RDEN];
-        }
-        misc[1] = num / den;
-        return;
-    }
-    if (mode == 0) {
-        // init: S = {sum p, sum p mu_m, sum p omega, sum p kappa, sum p lambda_m} over both classes
-        for (int L = 0; L <= N; L++) {
-            lam[L] = S[L][4];
-            mu[L] = S[L][1];
-            om[L] = S[L][2];
-            ka[L] = S[L][3];
-            blk[V2S_SUMP + L] = S[L][0];
-            blk[V2S_DL1 + L] = 0.0;
-        }
-        c = 0;   // the first half-sweep updates class 1
-    } else {
-        for (int L = 1; L <= N - 1; L++) {
-            if (!((active >> L) & 1u)) continue;
-            const double lnew = full_lists ? Lam * S[L][V2_P] : S[L][V2_LAM];
-            const double mstar = al[L] * lam[L - 1];
-            // Eq. muHeter via the exact flow identity sum_m p den = mu* + lambda_old(n)
-            const double mnew = mstar + lam[L] - lnew;
-            blk[V2S_MUSTAR + L] = mstar;
-            lam[L] = lnew;
-            mu[L] = mnew;
-            om[L] = S[L][V2_OM];
-            ka[L] = S[L][V2_KA];
-            blk[V2S_SUMP + L] = S[L][V2_P];
-            blk[V2S_DL1 + L] = S[L][V2_DL1];
-            if (!(S[L][V2_P] > 0.0) || !isfinite(mnew)) misc[0] = 1.0;
-        }
-    }
-    // coefficients for the next half-sweep (class 1 - c)
-    const int nc = 1 - c;
-    for (int L = 1; L <= N - 1; L++) {
-        if ((L & 1) != nc) continue;
-        const double b = lam[L] / mu[L + 1];
-        const double a = (1.0 - b * ka[L + 1]) / om[L - 1];
-        be[L] = b;
-        al[L] = a;
-        if (!(om[L - 1] > 0.0) || !isfinite(a) || !(a > 0.0)) misc[0] = 1.0;
-    }
-    // Eq. bnd_stationary
-    double prod = 1.0, tot = 1.0;
-    double g[HQ_NL];
-    g[0] = 1.0;
-    for (int L = 1; L <= N; L++) {
-        prod *= lam[L - 1] / mu[L];
-        g[L] = prod;
-        tot += prod;
-    }
-    pn1[0] = 0.0;
-    for (int L = 0; L <= N; L++) pn1[L + 1] = g[L] / tot;
-    for (int L = N + 2; L < 34; L++) pn1[L] = 0.0;
-    double prox = 0.0;
-    for (int L = 1; L <= N - 1; L++) prox += pn1[L + 1] * blk[V2S_DL1 + L];
-    misc[2] = prox;
+    // the scalar step runs on a shared-memory copy of the block (one thread, serial)
+    __shared__ double sblk[V2S_TOTAL];
+    for (int i = threadIdx.x; i < V2S_TOTAL; i += blockDim.x) sblk[i] = blk[i];
+    __syncthreads();
+    scalars_update(N, full_lists, Lam, mode, c, active, S, sblk);
+    for (int i = threadIdx.x; i < V2S_TOTAL; i += blockDim.x) blk[i] = sblk[i];
 }
 
 // pi[m_abi] = p(w(m)) p_{w(m)}(m), internal index m -> ABI index via perm.
@@ -819,8 +768,8 @@ cudaError_t prog_max(const uint32_t *size16, uint32_t *out, uint64_t n, void *tm
     return cub::DeviceReduce::Max(tmp, *tmp_bytes, size16, out, (int)n, s);
 }
 cudaError_t scalars(int N, int full_lists, double Lam, int mode, int c, uint32_t active, int ncta,
-                    const double *partial, double *blk, cudaStream_t s) {
-    hq2::k_scalars2<<<1, 1024, 0, s>>>(N, full_lists, Lam, mode, c, active, ncta, partial, blk);
+                    const double *partial, double *blk, cudaStream_t s, int transposed) {
+    hq2::k_scalars2<<<1, 1024, 0, s>>>(N, full_lists, Lam, mode, c, active, ncta, partial, blk, transposed);
     return cudaGetLastError();
 }
 cudaError_t assemble(int N, const double *pw, const double *pn1, const int *perm, double *pi, int grid,

@@ -39,10 +39,16 @@
 #include "hq_internal.h"
 #include "hq_v2.h"
 #include "hq_v3.h"
+#include "hq_scalars.cuh"
 
 namespace hq3 {
 
 constexpr int R = V3_R;
+#ifdef HQ_FUSED_SCALARS
+constexpr bool kFusedScalars = true;    // A/B variant: scalar step in the sweep kernel's last CTA
+#else
+constexpr bool kFusedScalars = false;   // scalar step as its own launch (k_scalars2): measured faster
+#endif
 
 __device__ __forceinline__ double warp_sum(double s) {
 #pragma unroll
@@ -590,6 +596,7 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
 #pragma unroll
     for (int v = 0; v < NB; v++) red[((size_t)warp * 32 + lane) * NB + v] = acc[v];
     __syncthreads();
+    const int G = gridDim.x;
     if (warp == 0) {
         double s[NB];
 #pragma unroll
@@ -597,12 +604,75 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
         for (int w = 0; w < (int)nwarps; w++)
 #pragma unroll
             for (int v = 0; v < NB; v++) s[v] += red[((size_t)w * 32 + lane) * NB + v];
-        double *out = a.partial + ((size_t)blockIdx.x * HQ_NL + lane) * HQ_NV;
+        if (MODE == 2) {
+            double *out = a.partial + ((size_t)blockIdx.x * HQ_NL + lane) * HQ_NV;
 #pragma unroll
-        for (int v = 0; v < HQ_NV; v++) out[v] = 0.0;
+            for (int v = 0; v < HQ_NV; v++) out[v] = 0.0;
 #pragma unroll
-        for (int v = 0; v < NB; v++) out[SL::slot(v)] = s[v];
+            for (int v = 0; v < NB; v++) out[SL::slot(v)] = s[v];
+        } else {   // transposed: partial[(layer * HQ_NV + slot) * G + cta]
+            double o[NV2];
+#pragma unroll
+            for (int v = 0; v < NV2; v++) o[v] = 0.0;
+#pragma unroll
+            for (int v = 0; v < NB; v++) o[SL::slot(v)] = s[v];
+#pragma unroll
+            for (int v = 0; v < NV2; v++) a.partial[((size_t)lane * HQ_NV + v) * G + blockIdx.x] = o[v];
+        }
     }
+    if (MODE == 2 || !kFusedScalars) return;
+    // ---- the last CTA to finish reduces the partials (fixed CTA order) and performs the
+    //      scalar step of the half-sweep (hq_scalars.cuh): no separate launch
+    __shared__ int s_last;
+    __shared__ double S[HQ_NL][NV2];
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = atomicAdd(a.done, 1u) == (unsigned)(G - 1);
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    // (layer, value) pair i = tid % 160 summed over CTA chunk tid / 160 (fixed order), then
+    // the chunks in order: all loads of a thread are independent and in flight together
+    {
+        constexpr int NP = HQ_NL * NV2;
+        const int nchunk = (int)blockDim.x / NP;   // 3 at 512 threads, 1 at >= 160 threads
+        double *cs = tileq;                        // [nchunk][NP]
+        if (nchunk >= 1 && tid < nchunk * NP) {
+            const int i = tid % NP, ch = tid / NP;
+            const int n = i / NV2, v = i - n * NV2;
+            const double *src = a.partial + ((size_t)n * HQ_NV + v) * G;
+            const int b0 = (G * ch) / nchunk, b1 = (G * (ch + 1)) / nchunk;
+            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+            int b = b0;
+            for (; b + 3 < b1; b += 4) {
+                s0 += __ldcg(src + b);
+                s1 += __ldcg(src + b + 1);
+                s2 += __ldcg(src + b + 2);
+                s3 += __ldcg(src + b + 3);
+            }
+            for (; b < b1; b++) s0 += __ldcg(src + b);
+            cs[ch * NP + i] = (s0 + s1) + (s2 + s3);
+        }
+        __syncthreads();
+        for (int i = tid; i < NP; i += blockDim.x) {
+            double s = 0.0;
+            if (nchunk >= 1) {
+                for (int ch = 0; ch < nchunk; ch++) s += cs[ch * NP + i];
+            } else {   // fewer than 160 threads: one pair at a time per thread
+                const int n = i / NV2, v = i - n * NV2;
+                const double *src = a.partial + ((size_t)n * HQ_NV + v) * G;
+                for (int b = 0; b < G; b++) s += __ldcg(src + b);
+            }
+            S[i / NV2][i % NV2] = s;
+        }
+    }
+    // the scalar step runs on a shared-memory copy of the block (one thread, serial)
+    double *sblk = tileq + 3 * HQ_NL * NV2;
+    for (int i = tid; i < V2S_TOTAL; i += blockDim.x) sblk[i] = __ldcg(a.blk + i);
+    __syncthreads();
+    scalars_update(a.N, a.full_lists, a.Lam, 1, a.c, a.active, S, sblk);
+    if (tid == 0) *a.done = 0u;
+    for (int i = tid; i < V2S_TOTAL; i += blockDim.x) a.blk[i] = sblk[i];
 }
 
 // ---------------------------------------------------------------------------
@@ -830,6 +900,8 @@ __global__ void k_prog_write3(P3Args a, const uint32_t *__restrict__ order, cons
 
 // ---------------------------------------------------------------------------
 namespace hq3_launch {
+
+bool fused_scalars() { return hq3::kFusedScalars; }
 
 int choose_nw(int N) {
     int nw = N - 9 - 8;   // keep >= 256 tiles while the CTA is narrower than 16 warps

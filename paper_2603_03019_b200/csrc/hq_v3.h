@@ -54,7 +54,10 @@ struct S3Args {
     double *P;               // updated class (sweep) / evaluated class (residual)
     const double2 *omkap;    // scatter weights of class c
     const double *coef;      // v2 scalar block (V2S_* offsets)
-    double *partial;         // [grid][HQ_NL][HQ_NV]
+    double *partial;         // MODE 2: [grid][HQ_NL][HQ_NV]; MODE 0/1: [HQ_NL][HQ_NV][grid]
+    double *blk;             // the scalar block, updated by the last CTA (MODE 0/1)
+    unsigned *done;          // CTA completion counter (self-resetting)
+    int full_lists;
 };
 
 struct P3Args {   // program precompute (per warp tile)
@@ -77,4 +80,5 @@ size_t sweep_smem(int nW, uint32_t maxblk16, int nslots);
 int choose_slots(int nW, uint32_t maxblk16);
 uint32_t choose_cap(int nW, uint32_t maxblk16);
 int choose_nw(int N);
+bool fused_scalars();
 }  // namespace hq3_launch

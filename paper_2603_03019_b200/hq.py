@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libhq.so")
+LIB_PATH = os.environ.get("HQ_LIB") or os.path.join(_PKG, "libhq.so")   # HQ_LIB: A/B variant builds (tools/ab.py)
 
 HQ_OK = 0
 HQ_NOT_CONVERGED = 1
@@ -189,7 +189,8 @@ class Solver:
     def stats(self):
         s = hq_stats(self.h)
         keys = ["sweeps", "halfsweeps", "state_updates", "launches", "residual_evals", "trie_nodes", "sum_pi_minus_1",
-                "solve_ms", "sweep_ms", "sweep_launches", "residual_ms", "precompute_ms", "program_bytes", "path"]
+                "solve_ms", "sweep_ms", "sweep_launches", "residual_ms", "precompute_ms", "program_bytes", "path",
+                "max_program_block", "staged_program_capacity"]
         return {k: float(s[i]) for i, k in enumerate(keys)}
 
     def close(self):

@@ -1,0 +1,58 @@
+"""A/B timing of library variants on the same GPU, interleaved.
+
+  python tools/ab.py build NAME [DEFINE ...]     (here: compile variants/libhq_NAME.so)
+  python tools/ab.py run CFG REPS NAME [NAME...] (GPU box: time hq_solve per variant)
+
+Each run creates a solver per variant, warms it up, then alternates variants for REPS
+rounds; prints the median solve time and sweep-kernel time of each.  Development aid."""
+import json
+import os
+import statistics
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+VAR = os.path.join(ROOT, "variants")
+
+if sys.argv[1] == "build":
+    sys.path.insert(0, ROOT)
+    from paper_2603_03019_b200 import build as b
+
+    os.makedirs(VAR, exist_ok=True)
+    b.build(out=os.path.join(VAR, f"libhq_{sys.argv[2]}.so"), defines=sys.argv[3:])
+    sys.exit(0)
+
+cfg, reps, names = int(sys.argv[2]), int(sys.argv[3]), sys.argv[4:]
+child = r'''
+import json, os, statistics, sys
+sys.path.insert(0, os.environ["ROOT"])
+import torch, hqinst
+from paper_2603_03019_b200 import hq
+inst = hqinst.config_instance(int(os.environ["CFG"]))
+s = hq.Solver.from_instance(inst)
+pi = torch.empty(1 << inst.N, dtype=torch.float64, device="cuda")
+for _ in range(2):
+    s.solve(tol=1e-13, max_iter=5000, pi=pi)
+out = []
+for _ in range(int(os.environ["REPS"])):
+    r = s.solve(tol=1e-13, max_iter=5000, pi=pi)
+    st = s.stats()
+    out.append((st["solve_ms"], st["sweep_ms"], r["iters"], r["residual"]))
+print(json.dumps(out))
+'''
+res = {n: [] for n in names}
+for rnd in range(2):   # two interleaved rounds of fresh processes
+    for n in names:
+        env = dict(os.environ, ROOT=ROOT, CFG=str(cfg), REPS=str(reps), HQ_LIB=os.path.join(VAR, f"libhq_{n}.so"))
+        p = subprocess.run([sys.executable, "-c", child], env=env, capture_output=True, text=True, timeout=600)
+        if p.returncode != 0:
+            print(n, "FAILED", p.stderr[-2000:])
+            continue
+        res[n] += json.loads(p.stdout.strip().splitlines()[-1])
+for n in names:
+    if not res[n]:
+        continue
+    solve = statistics.median(x[0] for x in res[n])
+    sweep = statistics.median(x[1] for x in res[n])
+    print(json.dumps(dict(variant=n, solve_ms=round(solve, 2), sweep_ms=round(sweep, 2), iters=res[n][0][2],
+                          residual=res[n][0][3], samples=len(res[n]))))
