@@ -607,8 +607,8 @@ static hq_status v2_prepare(hq_problem *h, cudaStream_t s) {
             x = (((r ^ x) >> 2) / cc) | r;
         }
     }
-    // path 3: rate programs are per warp tile, (t << nW) | w, stored tile by tile
-    const int nWp = h->path == 3 ? h->nW : 0;
+    // path 3: one rate program per CTA tile
+    const int nWp = 0;
     const uint64_t nprog = ntiles << nWp;
     if (nWp) {
         std::vector<uint32_t> w(nprog);
@@ -645,6 +645,7 @@ static hq_status v2_prepare(hq_problem *h, cudaStream_t s) {
     P3Args p3;
     memset(&p3, 0, sizeof(p3));
     p3.N = N;
+    p3.nW = h->nW;
     p3.full_lists = pa.full_lists;
     p3.ntiles = nprog;
     for (int u = 0; u < 32; u++) p3.nu[u] = pa.nu[u];
@@ -684,8 +685,8 @@ static hq_status v2_prepare(hq_problem *h, cudaStream_t s) {
             for (uint32_t x = 0; x < (1u << nWp); x++) b += sz[(i << nWp) | x];
             mb = std::max(mb, b);
             // estimated work of a tile in program-record units: the gather of its 2^(8+nW)
-            // states (~2048 records' worth at 16 warps) plus one record per program record
-            cost[i] = (double)(128u << nWp) + (double)b;
+            // states plus the evaluation of each program record by every warp
+            cost[i] = 256.0 + (double)b;
             tot += cost[i];
         }
         h->maxrec = mb;

@@ -162,37 +162,44 @@ __device__ __forceinline__ uint32_t ldpu(const uint32_t *p, uint64_t pol) {
     return v;
 }
 
-// Rate program of a warp tile (hq_v3.h): per unit either nothing (the warp-tile-uniform
-// rate W0[u] applies to every lane) or a data block: a table of the thread-level rate
-// (W0 plus the lane-conditioned pairs, summed at precompute time) over the lane bits M
+// Rate program of a CTA tile (hq_v3.h): per unit either nothing (the tile-uniform rate
+// W0[u] applies to every thread) or a data block: a table of the thread-level rate (W0
+// plus the lane/warp-conditioned pairs, summed at precompute time) over the thread bits M
 // its conditions use, then groups of register-dependent pairs, each a mask of admissible
-// register states and a table of their summed rate.  Entry of lane l: pext(l, M), looked
-// up in a 32 x 32 byte table.  The program block of a CTA tile is staged in shared memory
-// with the tile's q block (generic pointer: oversized blocks stay in global memory).
+// register states and a table of their summed rate.  Entry of thread (warp w, lane l):
+// pext(l, M & 31) | pext(w, M >> 5) << popc(M & 31), from two small shared tables.  The
+// block is staged in shared memory with the tile's q block (generic pointer: an oversized
+// block stays in global memory).
 struct Prog {
     const uint4 *pg;        // header
-    const uint8_t *pext;    // pext[M * 32 + lane]
-    uint32_t info;          // info[lane] (broadcast to the unit being processed by shuffles)
+    const uint8_t *pl;      // pl[M5 * 32] = pext(lane, M5) for this lane (stride 32)
+    const uint8_t *pw;      // pw[M4 * 16] = pext(warp, M4) for this warp (stride 16)
+    uint32_t info;          // info[lane]: (table << 31) | start << 8 | ngroups
+    uint32_t infm;          // M of the table of unit `lane`
     double w0;              // W0[lane]
     __device__ __forceinline__ double W0(int u) const { return __shfl_sync(0xffffffffu, w0, u); }
+    __device__ __forceinline__ uint32_t idx(uint32_t M) const {
+        return (uint32_t)pl[(M & 31u) * 32] | ((uint32_t)pw[(M >> 5) * 16] << __popc(M & 31u));
+    }
 };
 __device__ __forceinline__ double unit_rates(const Prog &P, int u, int lane, int sh, double w0,
                                              const double (&q)[R], double (&A)[R]) {
+    (void)lane;
     const uint32_t inf = __shfl_sync(0xffffffffu, P.info, u);
+    const uint32_t Mt = __shfl_sync(0xffffffffu, P.infm, u);
     if (!inf) return w0;
     const uint4 *d = P.pg + V3_HDR16 + ((inf >> 8) & 0xffffu);
     double Wt = w0;
     if (inf >> 31) {
-        const uint32_t M = (inf >> 24) & 0x1fu;
-        Wt = reinterpret_cast<const double *>(d)[P.pext[M * 32 + lane]];
-        d += ((1 << __popc(M)) + 1) >> 1;
+        Wt = reinterpret_cast<const double *>(d)[P.idx(Mt)];
+        d += ((1 << __popc(Mt)) + 1) >> 1;
     }
     const int ng = (int)(inf & 0xffu);
     for (int g = 0; g < ng; g++) {
         const uint32_t hd = d->x;
-        const uint32_t M = (hd >> 16) & 0x1fu;
+        const uint32_t M = (hd >> 16) & 0x1ffu;
         const uint32_t m8 = (hd >> sh) & 0xffu;
-        const double w = reinterpret_cast<const double *>(d + 1)[P.pext[M * 32 + lane]];
+        const double w = reinterpret_cast<const double *>(d + 1)[P.idx(M)];
         d += 1 + (((1 << __popc(M)) + 1) >> 1);
 #pragma unroll
         for (int r = 0; r < R; r++) pfma(A[r], w, q[r], m8 & (1u << r));
@@ -240,7 +247,8 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t tbar[2];
     __shared__ double s_x[32], s_y[32], s_z[32], s_mr[R];
-    __shared__ uint8_t s_pext[32 * 32];
+    __shared__ uint8_t s_pext[32 * 32];   // [M5][lane] = pext(lane, M5)
+    __shared__ uint8_t s_pextw[16 * 16];  // [M4][warp] = pext(warp, M4)
 
     const int nW = a.nW, T = 8 + nW, NVU = 9 + nW, nH = a.N - NVU;
     const int tid = threadIdx.x, lane = tid & 31, warp = wuni(tid >> 5);
@@ -275,6 +283,13 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
             if ((M >> b) & 1u) r |= ((l >> b) & 1u) << j++;
         s_pext[i] = (uint8_t)r;
     }
+    for (int i = tid; i < 16 * 16; i += blockDim.x) {
+        const uint32_t M = (uint32_t)i >> 4, w = (uint32_t)i & 15u;
+        uint32_t r = 0;
+        for (int b = 0, j = 0; b < 4; b++)
+            if ((M >> b) & 1u) r |= ((w >> b) & 1u) << j++;
+        s_pextw[i] = (uint8_t)r;
+    }
     if (tid == 0) {
         mbar_init(sptr(&tbar[0]), 1);
         mbar_init(sptr(&tbar[1]), 1);
@@ -286,14 +301,13 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
     // host so that every CTA gets the same estimated work
     const uint32_t i0 = __ldg(a.range + blockIdx.x), i1 = __ldg(a.range + blockIdx.x + 1);
     const int nt = (int)(i1 - i0);
-    const uint64_t nwt = (uint64_t)a.ntiles << nW;
 
     // ---- tile loader (thread 0): q block + program block of tile k, double-buffered
     auto load_tile = [&](int k) {
-        const uint64_t widx = (uint64_t)(i0 + k) << nW;
-        const uint32_t t = __ldg(a.order + widx) >> nW;
-        const uint32_t o = __ldg(a.off16 + widx);
-        const uint32_t nrec = (widx + nwarps < nwt ? __ldg(a.off16 + widx + nwarps) : a.total16) - o;
+        const uint32_t idx = i0 + k;
+        const uint32_t t = __ldg(a.order + idx);
+        const uint32_t o = __ldg(a.off16 + idx);
+        const uint32_t nrec = (idx + 1 < a.ntiles ? __ldg(a.off16 + idx + 1) : a.total16) - o;
         const bool staged = nrec <= a.maxblk16;
         const int buf = k & 1;
         const unsigned bar = sptr(&tbar[buf]);
@@ -306,10 +320,12 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
     if (tid == 0 && nt > 0) load_tile(0);
 
     // ---- per-thread constants
-    double mu_t = 0.0;
+    double mu_t = 0.0;   // busy lane and warp units of this thread (tile units: mu_F of the program)
 #pragma unroll
     for (int b = 0; b < 5; b++)
         if ((lane >> b) & 1) mu_t += a.nu[2 + b];
+    for (int b = 0; b < nW; b++)
+        if ((warp >> b) & 1) mu_t += a.nu[9 + b];
     const int popc_t = __popc(lane) + __popc(warp);
     const int par_t = popc_t & 1;
     const uint32_t jw = ((uint32_t)warp << 8) | ((uint32_t)lane << 1);   // j_local(r) = jw | (r>>1)<<6 | (r&1)
@@ -358,8 +374,8 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
     };
 
     for (int k = 0; k < nt; k++) {
-        const uint64_t widx = (uint64_t)(i0 + k) << nW;
-        const uint32_t t = __ldg(a.order + widx) >> nW;
+        const uint32_t tidx = i0 + k;
+        const uint32_t t = __ldg(a.order + tidx);
         const uint32_t jt = t << T;
         const int buf = k & 1;
         // tile-unit neighbour slices: two units of loads in flight ahead of the one accumulated
@@ -382,11 +398,13 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
         const double *tq = tileq + (size_t)buf * BUFD;
         Prog P;
         {
-            const uint32_t o0 = __ldg(a.off16 + widx), ow = __ldg(a.off16 + widx + warp);
-            const uint32_t nrec = (widx + nwarps < nwt ? __ldg(a.off16 + widx + nwarps) : a.total16) - o0;
-            P.pg = nrec <= a.maxblk16 ? reinterpret_cast<const uint4 *>(tq + TS) + (ow - o0) : a.prog + ow;
-            P.pext = s_pext;
+            const uint32_t o0 = __ldg(a.off16 + tidx);
+            const uint32_t nrec = (tidx + 1 < a.ntiles ? __ldg(a.off16 + tidx + 1) : a.total16) - o0;
+            P.pg = nrec <= a.maxblk16 ? reinterpret_cast<const uint4 *>(tq + TS) : a.prog + o0;
+            P.pl = s_pext + lane;
+            P.pw = s_pextw + warp;
             P.info = reinterpret_cast<const uint32_t *>(P.pg)[lane];
+            P.infm = reinterpret_cast<const uint32_t *>(P.pg + 25)[lane];
             P.w0 = reinterpret_cast<const double *>(P.pg + 8)[lane];
         }
         const int K = __popc(t);
@@ -729,10 +747,23 @@ __device__ uint32_t reg_mask(int u, uint32_t S, bool pseudo) {
     return rm;
 }
 
+// thread-level condition bits of a pattern S: lane units 2..6 -> bits 0..4, warp units
+// 9..8+nW -> bits 5..8 (the index space of a table)
+__device__ __forceinline__ uint32_t cond_bits(const P3Args &a, uint32_t S) {
+    return ((S >> 2) & 0x1fu) | (((S >> 9) & ((1u << a.nW) - 1u)) << 5);
+}
+// own busy condition of a lane / warp unit (its table is zero where it is free)
+__device__ __forceinline__ uint32_t own_bits(const P3Args &a, int u) {
+    if (u == a.N) return 0u;
+    if (u >= 2 && u <= 6) return 1u << (u - 2);
+    if (u >= 9 && u < 9 + a.nW) return 1u << (u - 9 + 5);
+    return 0u;
+}
+
 // Walk the trie for tile t, then sort the pairs by (unit, class, rm).
 // Returns the number of 16-byte records after the header, or -1 on overflow.
 __device__ int tile_program(const P3Args &a, uint32_t t, double *W0, PairAcc3 &P) {
-    const int NVU = 9;
+    const int NVU = 9 + a.nW;
     uint32_t Sst[HQ_MAXN + 2];
     Sst[0] = 0;
     for (int u = 0; u <= HQ_MAXN; u++) W0[u] = 0.0;
@@ -781,17 +812,17 @@ __device__ int tile_program(const P3Args &a, uint32_t t, double *W0, PairAcc3 &P
         P.val[y + 1] = vx;
         P.rm[y + 1] = mx;
     }
-    // records: per unit with data: a lane table if it has lane-only pairs, then one group
-    // per distinct rm; a table over the lane bits M its conditions use has 2^|M| entries
-    // (ceil(2^|M| / 2) records); a group adds one header record
+    // records: per unit with data: a table if it has thread-conditioned pairs, then one
+    // group per distinct rm; a table over the lane/warp bits M its conditions use has
+    // 2^|M| entries (ceil(2^|M| / 2) records); a group adds one header record
     int nrec = 0;
     int k = 0;
     while (k < P.n) {
         const int u = (int)(P.key[k] & 63);
         const uint16_t rm = P.rm[k];
-        uint32_t M = (!(u == a.N) && u >= 2 && u <= 6) ? (1u << (u - 2)) : 0u;
+        uint32_t M = own_bits(a, u);
         while (k < P.n && (int)(P.key[k] & 63) == u && P.rm[k] == rm) {
-            M |= (P.key[k] >> 8) & 0x1fu;   // lane units 2..6 of S -> lane bits 0..4
+            M |= cond_bits(a, P.key[k] >> 6);
             k++;
         }
         nrec += (rm ? 1 : 0) + (((1 << __popc(M)) + 1) >> 1);
@@ -815,9 +846,9 @@ __global__ void k_prog_count3(P3Args a, const uint32_t *__restrict__ order, uint
     }
 }
 
-__device__ __forceinline__ uint32_t pdep5(uint32_t idx, uint32_t M) {   // deposit idx bits into the set bits of M
+__device__ __forceinline__ uint32_t pdep9(uint32_t idx, uint32_t M) {   // deposit idx bits into the set bits of M
     uint32_t r = 0;
-    for (int b = 0, i = 0; b < 5; b++)
+    for (int b = 0, i = 0; b < 9; b++)
         if ((M >> b) & 1u) r |= ((idx >> i++) & 1u) << b;
     return r;
 }
@@ -826,33 +857,33 @@ __global__ void k_prog_write3(P3Args a, const uint32_t *__restrict__ order, cons
                               uint4 *__restrict__ prog, int *__restrict__ err) {
     PairAcc3 P;
     double W0[HQ_MAXN + 1];
-    const int NVU = 9;
+    const int NVU = 9 + a.nW;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.ntiles;
          i += (uint64_t)gridDim.x * blockDim.x) {
         uint4 *out = prog + off16[i];
         const uint32_t t = order[i];
         if (tile_program(a, t, W0, P) < 0) continue;
-        uint32_t info[32];
-        for (int q = 0; q < 32; q++) info[q] = 0u;
+        uint32_t info[32], infm[32];
+        for (int q = 0; q < 32; q++) info[q] = infm[q] = 0u;
         uint4 *data = out + V3_HDR16;
         uint32_t pos = 0;   // data records written
         int k = 0;
         while (k < P.n) {
             const int u = (int)(P.key[k] & 63);
-            const bool lane_unit = (u != a.N) && u >= 2 && u <= 6;
+            const uint32_t own = own_bits(a, u);
             const uint32_t start = pos;
             uint32_t inf = 0u, ng = 0u;
             while (k < P.n && (int)(P.key[k] & 63) == u) {
                 const uint16_t rm = P.rm[k];
                 const int k0 = k;
-                uint32_t M = lane_unit ? (1u << (u - 2)) : 0u;
+                uint32_t M = own;
                 while (k < P.n && (int)(P.key[k] & 63) == u && P.rm[k] == rm) {
-                    M |= (P.key[k] >> 8) & 0x1fu;
+                    M |= cond_bits(a, P.key[k] >> 6);
                     k++;
                 }
-                // table over the lane bits M: entry idx holds the value of every lane whose
-                // M-bits are pdep(idx, M); a pair applies when its lane units (and, for a
-                // lane unit, the unit itself) are busy in the lane
+                // table over the thread bits M: entry idx holds the value of every thread
+                // whose M-bits are pdep(idx, M); a pair applies when its lane / warp units
+                // (and, for a lane or warp unit, the unit itself) are busy for the thread
                 double *tab;
                 if (rm) {
                     data[pos] = make_uint4((uint32_t)rm | (M << 16), 0u, 0u, 0u);
@@ -861,18 +892,17 @@ __global__ void k_prog_write3(P3Args a, const uint32_t *__restrict__ order, cons
                     ng++;
                 } else {
                     tab = reinterpret_cast<double *>(data + pos);
-                    inf |= (1u << 31) | (M << 24);
+                    inf |= 1u << 31;
+                    infm[u] = M;
                 }
                 const int ne = 1 << __popc(M);
                 for (int idx = 0; idx < ne; idx++) {
-                    const uint32_t lanebits = pdep5((uint32_t)idx, M);
-                    const uint32_t busy = lanebits << 2;
+                    const uint32_t tb = pdep9((uint32_t)idx, M);   // thread bits: lanes 0..4, warps 5..8
                     double w = 0.0;
-                    if (!rm) w = (lane_unit && !((busy >> u) & 1u)) ? 0.0 : W0[u];
+                    if (!rm) w = (own && !(tb & own)) ? 0.0 : W0[u];
                     for (int kk = k0; kk < k; kk++) {
-                        uint32_t St = (P.key[kk] >> 6) & 0x7cu;
-                        if (lane_unit) St |= 1u << u;
-                        if ((St & ~busy) == 0u) w += P.val[kk];
+                        const uint32_t St = cond_bits(a, P.key[kk] >> 6) | own;
+                        if ((St & ~tb) == 0u) w += P.val[kk];
                     }
                     tab[idx] = w;
                 }
@@ -883,6 +913,8 @@ __global__ void k_prog_write3(P3Args a, const uint32_t *__restrict__ order, cons
             info[u] = inf | ng | (start << 8);
         }
         for (int q = 0; q < 8; q++) out[q] = make_uint4(info[4 * q], info[4 * q + 1], info[4 * q + 2], info[4 * q + 3]);
+        for (int q = 0; q < 8; q++)
+            out[25 + q] = make_uint4(infm[4 * q], infm[4 * q + 1], infm[4 * q + 2], infm[4 * q + 3]);
         double *w0o = reinterpret_cast<double *>(out + 8);
         for (int u = 0; u < 32; u++) w0o[u] = u <= HQ_MAXN ? W0[u] : 0.0;
         double muF = 0.0;

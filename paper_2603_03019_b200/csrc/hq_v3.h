@@ -19,7 +19,7 @@
 
 #define V3_R 8                 // states per thread
 #define V3_MAXSLOTS 8          // CTA ring slots (one tile-sized block each)
-#define V3_HDR16 25            // program header: info[32] (u32), W0[32] (f64), {mu_F, 0}
+#define V3_HDR16 33            // program header: info[32] (u32), W0[32] (f64), {mu_F, has}, M[32] (u32)
 #define V3_MAXPAIRS 1024
 
 // program record of a warp tile (16-byte units):
@@ -60,8 +60,9 @@ struct S3Args {
     int full_lists;
 };
 
-struct P3Args {   // program precompute (per warp tile)
+struct P3Args {   // program precompute (per CTA tile)
     int N;
+    int nW;
     int full_lists;
     uint64_t ntiles;
     double nu[32];           // internal-order service rates (mu_F in the header)
