@@ -134,7 +134,8 @@ const char *hq_error_string(hq_handle h);
  *   precompute time in ms (rate programs, scatter weights), [12] bytes of
  *   rate programs, [13] code path (1: N < 8 two-pass, 2: warp-tiled, 3: CTA-tiled),
  *   [14] largest rate-program block of a CTA tile (16-byte records),
- *   [15] staged program capacity (records; larger blocks are read from global memory).
+ *   [15] warp bits varying inside a rate program (0: one program per warp tile,
+ *        nW: one program per CTA tile; chosen by timing both at the first solve).
  */
 #define HQ_STATS_LEN 16
 hq_status hq_stats(hq_handle h, double *out);

@@ -309,6 +309,8 @@ struct hq_problem {
     int nslots = 0;                // path 3: CTA ring slots
     uint32_t maxblk_all = 0;       // path 3: largest program block of a CTA tile (records)
     unsigned *d_done = nullptr;    // path 3: CTA completion counter of the fused scalar step
+    int prog_nwv = 0;              // path 3: warp bits varying inside a rate program (nW: CTA programs)
+    float tune_ms[2] = {0.f, 0.f}; // path 3: timed sweeps with CTA / warp programs (0: not tuned)
     uint32_t *d_order = nullptr, *d_off16 = nullptr, *d_size16 = nullptr, *d_range = nullptr;
     uint4 *d_prog = nullptr;
     double2 *d_omkap = nullptr;
@@ -754,6 +756,302 @@ static hq_status v2_prepare(hq_problem *h, cudaStream_t s) {
     return HQ_OK;
 }
 
+// ---------------------------------------------------------------------------
+// path 3 preparation: rate programs at warp-tile or CTA-tile granularity (hq_v3.h)
+// ---------------------------------------------------------------------------
+struct ProgSet {
+    uint32_t *off16 = nullptr;   // [ntiles << nW] per-warp program offsets
+    uint32_t *range = nullptr;   // [grid + 1] CTA tile ranges
+    uint4 *prog = nullptr;
+    uint32_t total16 = 0, maxblk = 0, cap = 0;
+    int nwv = 0;
+    void release() {
+        cudaFree(off16);
+        cudaFree(range);
+        cudaFree(prog);
+        off16 = range = nullptr;
+        prog = nullptr;
+    }
+};
+
+static hq_status v3_programs(hq_problem *h, cudaStream_t s, int nwv, const std::vector<uint32_t> &order,
+                             ProgSet &ps) {
+    const int N = h->N, nW = h->nW;
+    const uint64_t ntiles = order.size(), W = 1ull << nW;
+    const bool per_warp = (nwv == 0 && nW > 0);
+    const uint64_t nprog = per_warp ? ntiles << nW : ntiles;
+    std::vector<uint32_t> pord(nprog);
+    for (uint64_t i = 0; i < ntiles; i++) {
+        if (per_warp)
+            for (uint64_t w = 0; w < W; w++) pord[(i << nW) | w] = (order[i] << nW) | (uint32_t)w;
+        else
+            pord[i] = order[i];
+    }
+    uint32_t *d_pord = nullptr, *d_size = nullptr, *d_offp = nullptr, *d_max = nullptr;
+    void *tmp = nullptr;
+    auto cleanup = [&]() {
+        cudaFree(d_pord);
+        cudaFree(d_size);
+        cudaFree(d_offp);
+        cudaFree(d_max);
+        cudaFree(tmp);
+    };
+    if (cudaMalloc((void **)&d_pord, 4 * nprog) != cudaSuccess || cudaMalloc((void **)&d_size, 4 * nprog) != cudaSuccess ||
+        cudaMalloc((void **)&d_offp, 4 * nprog) != cudaSuccess) {
+        cudaGetLastError();
+        cleanup();
+        h->err = "device memory for the rate-program tables could not be allocated";
+        return HQ_E_NOMEM;
+    }
+    HQ_CUDA(cudaMemcpyAsync(d_pord, pord.data(), 4 * nprog, cudaMemcpyHostToDevice, s));
+    P3Args p3;
+    memset(&p3, 0, sizeof(p3));
+    p3.N = N;
+    p3.nW = nW;
+    p3.nwv = nwv;
+    p3.full_lists = h->full_lists ? 1 : 0;
+    p3.ntiles = nprog;
+    for (int u = 0; u < 32; u++) p3.nu[u] = u < N ? h->nu_int[u] : 0.0;
+    p3.nnodes = (int)h->trie.node.size();
+    p3.node = h->d_node;
+    p3.lam_thr = h->d_lthr;
+    p3.lam_end = h->d_lend;
+    const int g = h->nsm * 8;
+    HQ_CUDA(cudaMemsetAsync(h->d_err, 0, sizeof(int), s));
+    HQ_CUDA(hq3_launch::prog_count(p3, d_pord, d_size, h->d_err, g, s));
+    size_t tb = 0;
+    HQ_CUDA(hq2_launch::prog_scan(d_size, d_offp, nprog, nullptr, &tb, s));
+    HQ_CUDA(cudaMalloc(&tmp, tb ? tb : 16));
+    HQ_CUDA(hq2_launch::prog_scan(d_size, d_offp, nprog, tmp, &tb, s));
+    std::vector<uint32_t> sz(nprog), offp(nprog);
+    int herr = 0;
+    HQ_CUDA(cudaMemcpyAsync(sz.data(), d_size, 4 * nprog, cudaMemcpyDeviceToHost, s));
+    HQ_CUDA(cudaMemcpyAsync(offp.data(), d_offp, 4 * nprog, cudaMemcpyDeviceToHost, s));
+    HQ_CUDA(cudaMemcpyAsync(&herr, h->d_err, sizeof(int), cudaMemcpyDeviceToHost, s));
+    HQ_CUDA(cudaStreamSynchronize(s));
+    if (herr) {
+        cleanup();
+        h->err = "rate program overflow (too many distinct (unit, pattern) pairs in a tile)";
+        return HQ_E_NUMERIC;
+    }
+    const uint64_t total16 = (uint64_t)offp[nprog - 1] + sz[nprog - 1];
+    if (total16 >= (1ull << 32)) {
+        cleanup();
+        h->err = "rate programs exceed 64 GB";
+        return HQ_E_NOMEM;
+    }
+    ps.release();
+    ps.nwv = nwv;
+    ps.total16 = (uint32_t)total16;
+    if (cudaMalloc((void **)&ps.prog, 16 * (total16 ? total16 : 1)) != cudaSuccess ||
+        cudaMalloc((void **)&ps.off16, 4 * (ntiles << nW)) != cudaSuccess) {
+        cudaGetLastError();
+        cleanup();
+        ps.release();
+        h->err = "device memory for the rate programs could not be allocated";
+        return HQ_E_NOMEM;
+    }
+    HQ_CUDA(hq3_launch::prog_write(p3, d_pord, d_offp, ps.prog, h->d_err, g, s));
+    // per-warp program offsets (a CTA program serves every warp of its tile), block sizes,
+    // work-balanced CTA ranges over the popcount-sorted tile order
+    std::vector<uint32_t> off16(ntiles << nW);
+    std::vector<double> cost(ntiles);
+    double tot = 0.0;
+    ps.maxblk = 0;
+    for (uint64_t i = 0; i < ntiles; i++) {
+        uint32_t b = 0;
+        for (uint64_t w = 0; w < W; w++) {
+            off16[(i << nW) | w] = per_warp ? offp[(i << nW) | w] : offp[i];
+            if (per_warp) b += sz[(i << nW) | w];
+        }
+        if (!per_warp) b = sz[i];
+        ps.maxblk = std::max(ps.maxblk, b);
+        // estimated work of a tile in program-record units: the gather of its states plus
+        // the evaluation of the program records (every warp evaluates a CTA program)
+        cost[i] = 256.0 + (double)b * (per_warp ? 1.0 : (double)W / 4.0);
+        tot += cost[i];
+    }
+    HQ_CUDA(cudaMemcpyAsync(ps.off16, off16.data(), 4 * off16.size(), cudaMemcpyHostToDevice, s));
+    const int G = h->sgrid;
+    std::vector<uint32_t> range(G + 1, (uint32_t)ntiles);
+    range[0] = 0;
+    double acc = 0.0;
+    int b = 1;
+    for (uint64_t i = 0; i < ntiles && b < G; i++) {
+        acc += cost[i];
+        while (b < G && acc >= tot * b / G) range[b++] = (uint32_t)(i + 1);
+    }
+    HQ_CUDA(cudaMalloc((void **)&ps.range, 4 * (G + 1)));
+    HQ_CUDA(cudaMemcpyAsync(ps.range, range.data(), 4 * (G + 1), cudaMemcpyHostToDevice, s));
+    HQ_CUDA(cudaMemcpyAsync(&herr, h->d_err, sizeof(int), cudaMemcpyDeviceToHost, s));
+    HQ_CUDA(cudaStreamSynchronize(s));
+    cleanup();
+    if (herr) {
+        ps.release();
+        h->err = "rate program overflow (more than 255 groups for a unit)";
+        return HQ_E_NUMERIC;
+    }
+    ps.cap = hq3_launch::choose_cap(nW, ps.maxblk);
+    return HQ_OK;
+}
+
+static void use_progset(hq_problem *h, ProgSet &ps) {
+    cudaFree(h->d_off16);
+    cudaFree(h->d_range);
+    cudaFree(h->d_prog);
+    h->d_off16 = ps.off16;
+    h->d_range = ps.range;
+    h->d_prog = ps.prog;
+    h->total16 = ps.total16;
+    h->maxblk_all = ps.maxblk;
+    h->maxrec = ps.cap;
+    h->prog_nwv = ps.nwv;
+    h->prog_bytes = 16.0 * (double)ps.total16;
+    ps.off16 = ps.range = nullptr;
+    ps.prog = nullptr;
+}
+
+static cudaError_t tiled_sweep(hq_problem *h, const S2Args &sa, int mode, cudaStream_t s);
+static S2Args base_s2(hq_problem *h);
+
+// time MODE-0 sweep launches with the programs now installed (the iterate is garbage:
+// timing only; hq_solve re-initialises everything afterwards)
+static hq_status v3_time_sweep(hq_problem *h, cudaStream_t s, float *ms) {
+    S2Args sa = base_s2(h);
+    const uint64_t half = 1ull << (h->N - 1);
+    sa.c = 1;
+    sa.active = 0xaaaaaaaau & ((1u << h->N) - 2u);
+    sa.P = h->d_pw + half;
+    sa.Q = h->d_pw;
+    sa.omkap = h->d_omkap + half;
+    cudaEvent_t e0 = h->event(0), e1 = h->event(1);
+    HQ_CUDA(tiled_sweep(h, sa, 0, s));
+    HQ_CUDA(cudaEventRecord(e0, s));
+    for (int i = 0; i < 2; i++) HQ_CUDA(tiled_sweep(h, sa, 0, s));
+    HQ_CUDA(cudaEventRecord(e1, s));
+    HQ_CUDA(cudaEventSynchronize(e1));
+    cudaEventElapsedTime(ms, e0, e1);
+    return HQ_OK;
+}
+
+static hq_status v3_prepare(hq_problem *h, cudaStream_t s) {
+    if (h->v2_ready) return HQ_OK;
+    const int N = h->N;
+    const uint64_t S = 1ull << N;
+    const int Nt = N - 9 - h->nW;
+    const uint64_t ntiles = 1ull << Nt;
+    // CTA tile visit order: by popcount of the tile index, ascending within a popcount class
+    std::vector<uint32_t> order;
+    order.reserve(ntiles);
+    order.push_back(0);
+    for (int K = 1; K <= Nt; K++) {
+        uint64_t x = (1ull << K) - 1;
+        while (x < ntiles) {
+            order.push_back((uint32_t)x);
+            const uint64_t cc = x & (~x + 1), r = x + cc;
+            x = (((r ^ x) >> 2) / cc) | r;
+        }
+    }
+    if (cudaMalloc((void **)&h->d_order, 4 * ntiles) != cudaSuccess ||
+        (!h->full_lists && cudaMalloc((void **)&h->d_lamarr, 8 * S) != cudaSuccess)) {
+        cudaGetLastError();
+        h->err = "device memory for the tile tables could not be allocated";
+        return HQ_E_NOMEM;
+    }
+    HQ_CUDA(cudaMemcpyAsync(h->d_order, order.data(), 4 * ntiles, cudaMemcpyHostToDevice, s));
+    P2Args pa;
+    memset(&pa, 0, sizeof(pa));
+    pa.N = N;
+    pa.full_lists = h->full_lists ? 1 : 0;
+    pa.Lam = h->Lam;
+    for (int u = 0; u < 32; u++) pa.nu[u] = u < N ? h->nu_int[u] : 0.0;
+    pa.nnodes = (int)h->trie.node.size();
+    pa.node = h->d_node;
+    pa.lam_thr = h->d_lthr;
+    pa.lam_end = h->d_lend;
+    cudaEvent_t e0 = h->event(2), e1 = h->event(3);
+    HQ_CUDA(cudaEventRecord(e0, s));
+    const int g = h->nsm * 8;
+    if (!h->full_lists) HQ_CUDA(hq2_launch::lambda_states(pa, h->d_lamarr, g, s));
+    HQ_CUDA(hq2_launch::omkap(pa, h->d_lamarr, h->d_omkap, g, s));
+    if (!h->d_done) {
+        HQ_CUDA(cudaMalloc((void **)&h->d_done, sizeof(unsigned)));
+        HQ_CUDA(cudaMemsetAsync(h->d_done, 0, sizeof(unsigned), s));
+    }
+    // program granularity: CTA programs (warps share one program; balanced) or warp
+    // programs (warp bits folded; fewer pairs per thread).  HQ_PROG=cta|warp forces one;
+    // otherwise both are built and the faster sweep is kept.
+    const char *env = getenv("HQ_PROG");
+    const std::string pref = env ? env : "";
+    ProgSet a, b;
+    hq_status st;
+    if (pref == "warp" || h->nW == 0) {
+        st = v3_programs(h, s, 0, order, a);
+        if (st != HQ_OK) return st;
+    } else if (pref == "cta") {
+        st = v3_programs(h, s, h->nW, order, a);
+        if (st != HQ_OK) return st;
+    } else {
+        float tc = INFINITY, tw = INFINITY;
+        st = v3_programs(h, s, h->nW, order, a);
+        if (st == HQ_OK) {
+            use_progset(h, a);
+            st = v3_time_sweep(h, s, &tc);
+            if (st != HQ_OK) return st;
+        } else if (st != HQ_E_NUMERIC) {
+            return st;
+        }
+        st = v3_programs(h, s, 0, order, b);
+        if (st != HQ_OK) return st;
+        if (std::isfinite(tc)) {
+            ProgSet cur;   // take back the CTA set
+            cur.off16 = h->d_off16;
+            cur.range = h->d_range;
+            cur.prog = h->d_prog;
+            cur.total16 = h->total16;
+            cur.maxblk = h->maxblk_all;
+            cur.cap = h->maxrec;
+            cur.nwv = h->prog_nwv;
+            h->d_off16 = nullptr;
+            h->d_range = nullptr;
+            h->d_prog = nullptr;
+            use_progset(h, b);
+            st = v3_time_sweep(h, s, &tw);
+            if (st != HQ_OK) return st;
+            h->tune_ms[0] = tc;
+            h->tune_ms[1] = tw;
+            if (tc < tw) {
+                ProgSet w;
+                w.off16 = h->d_off16;
+                w.range = h->d_range;
+                w.prog = h->d_prog;
+                h->d_off16 = nullptr;
+                h->d_range = nullptr;
+                h->d_prog = nullptr;
+                w.release();
+                use_progset(h, cur);
+            } else {
+                cur.release();
+            }
+        }
+        a = ProgSet();
+        b = ProgSet();
+    }
+    if (a.prog) use_progset(h, a);
+    h->nslots = hq3_launch::choose_slots(h->nW, h->maxrec);
+    if (h->nslots < 1) {
+        h->err = "tile working set exceeds the shared-memory budget";
+        return HQ_E_NUMERIC;
+    }
+    HQ_CUDA(cudaEventRecord(e1, s));
+    HQ_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    h->precompute_ms = ms;
+    h->v2_ready = true;
+    return HQ_OK;
+}
+
 // one sweep / residual launch of the tiled paths (2: hq_v2.cu, 3: hq_v3.cu)
 static cudaError_t tiled_sweep(hq_problem *h, const S2Args &sa, int mode, cudaStream_t s) {
     if (h->path != 3) return hq2_launch::sweep(sa, mode, h->sgrid, s);
@@ -783,6 +1081,25 @@ static cudaError_t tiled_sweep(hq_problem *h, const S2Args &sa, int mode, cudaSt
     a.coef = sa.coef;
     a.partial = sa.partial;
     return hq3_launch::sweep(a, sa.full_lists, mode, h->sgrid, s);
+}
+
+static S2Args base_s2(hq_problem *h) {
+    const int N = h->N;
+    S2Args sa;
+    memset(&sa, 0, sizeof(sa));
+    sa.N = N;
+    sa.full_lists = h->full_lists ? 1 : 0;
+    sa.ntiles = 1ull << (h->path == 3 ? N - 9 - h->nW : N - 8);
+    sa.Lam = h->Lam;
+    for (int u = 0; u < 32; u++) sa.nu[u] = u < N ? h->nu_int[u] : 0.0;
+    sa.order = h->d_order;
+    sa.off16 = h->d_off16;
+    sa.prog = h->d_prog;
+    sa.total16 = h->total16;
+    sa.maxrec = h->maxrec;
+    sa.coef = h->d_blk;
+    sa.partial = h->d_partial;
+    return sa;
 }
 
 struct SolveOut {
@@ -817,7 +1134,7 @@ static hq_status v2_residual(hq_problem *h, cudaStream_t s, S2Args sa, SolveOut 
 }
 
 static hq_status solve_v2(hq_problem *h, double tol, int max_iter, double *pi, cudaStream_t s, SolveOut &o) {
-    hq_status st = v2_prepare(h, s);
+    hq_status st = h->path == 3 ? v3_prepare(h, s) : v2_prepare(h, s);
     if (st != HQ_OK) return st;
     const int N = h->N;
     const uint64_t half = 1ull << (N - 1);
@@ -842,20 +1159,7 @@ static hq_status solve_v2(hq_problem *h, double tol, int max_iter, double *pi, c
         return HQ_OK;
     }
 
-    S2Args sa;
-    memset(&sa, 0, sizeof(sa));
-    sa.N = N;
-    sa.full_lists = h->full_lists ? 1 : 0;
-    sa.ntiles = 1ull << (h->path == 3 ? N - 9 - h->nW : N - 8);
-    sa.Lam = h->Lam;
-    for (int u = 0; u < 32; u++) sa.nu[u] = u < N ? h->nu_int[u] : 0.0;
-    sa.order = h->d_order;
-    sa.off16 = h->d_off16;
-    sa.prog = h->d_prog;
-    sa.total16 = h->total16;
-    sa.maxrec = h->maxrec;
-    sa.coef = h->d_blk;
-    sa.partial = h->d_partial;
+    S2Args sa = base_s2(h);
 
     // convergence checks: the two half-sweeps before a check record |dp|
     int next_check = N + 2 * 12;
@@ -992,7 +1296,7 @@ extern "C" hq_status hq_solve(hq_handle h, double tol, int max_iter, double *pi,
         h->stats[12] = h->prog_bytes;
         h->stats[13] = h->path;   // path id
         h->stats[14] = h->maxblk_all;
-        h->stats[15] = h->maxrec;
+        h->stats[15] = h->prog_nwv;
         if (iters_out) *iters_out = o.sweeps;
         if (residual_out) *residual_out = o.res;
         if (!std::isfinite(o.res)) {

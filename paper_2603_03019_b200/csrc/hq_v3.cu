@@ -303,11 +303,12 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
     const int nt = (int)(i1 - i0);
 
     // ---- tile loader (thread 0): q block + program block of tile k, double-buffered
+    const uint64_t nwt = (uint64_t)a.ntiles << nW;   // per-warp program slots
     auto load_tile = [&](int k) {
-        const uint32_t idx = i0 + k;
-        const uint32_t t = __ldg(a.order + idx);
-        const uint32_t o = __ldg(a.off16 + idx);
-        const uint32_t nrec = (idx + 1 < a.ntiles ? __ldg(a.off16 + idx + 1) : a.total16) - o;
+        const uint64_t widx = (uint64_t)(i0 + k) << nW;
+        const uint32_t t = __ldg(a.order + (i0 + k));
+        const uint32_t o = __ldg(a.off16 + widx);
+        const uint32_t nrec = (widx + nwarps < nwt ? __ldg(a.off16 + widx + nwarps) : a.total16) - o;
         const bool staged = nrec <= a.maxblk16;
         const int buf = k & 1;
         const unsigned bar = sptr(&tbar[buf]);
@@ -398,9 +399,10 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
         const double *tq = tileq + (size_t)buf * BUFD;
         Prog P;
         {
-            const uint32_t o0 = __ldg(a.off16 + tidx);
-            const uint32_t nrec = (tidx + 1 < a.ntiles ? __ldg(a.off16 + tidx + 1) : a.total16) - o0;
-            P.pg = nrec <= a.maxblk16 ? reinterpret_cast<const uint4 *>(tq + TS) : a.prog + o0;
+            const uint64_t widx = (uint64_t)tidx << nW;
+            const uint32_t o0 = __ldg(a.off16 + widx), ow = __ldg(a.off16 + widx + warp);
+            const uint32_t nrec = (widx + nwarps < nwt ? __ldg(a.off16 + widx + nwarps) : a.total16) - o0;
+            P.pg = nrec <= a.maxblk16 ? reinterpret_cast<const uint4 *>(tq + TS) + (ow - o0) : a.prog + ow;
             P.pl = s_pext + lane;
             P.pw = s_pextw + warp;
             P.info = reinterpret_cast<const uint32_t *>(P.pg)[lane];
@@ -697,7 +699,7 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
 // Rate-program precompute (once per instance): Algorithm 3
 // walked symbolically over the tile's varying units.
 // ---------------------------------------------------------------------------
-constexpr int MAXP = V3_MAXPAIRS;
+constexpr int MAXP = V3_MAXPAIRS;   // distinct (unit, pattern) pairs of one program
 constexpr uint32_t PRMASK = 1u | (1u << 1) | (1u << 7) | (1u << 8);   // parity + register units
 
 struct PairAcc3 {
@@ -750,20 +752,20 @@ __device__ uint32_t reg_mask(int u, uint32_t S, bool pseudo) {
 // thread-level condition bits of a pattern S: lane units 2..6 -> bits 0..4, warp units
 // 9..8+nW -> bits 5..8 (the index space of a table)
 __device__ __forceinline__ uint32_t cond_bits(const P3Args &a, uint32_t S) {
-    return ((S >> 2) & 0x1fu) | (((S >> 9) & ((1u << a.nW) - 1u)) << 5);
+    return ((S >> 2) & 0x1fu) | (((S >> 9) & ((1u << a.nwv) - 1u)) << 5);
 }
 // own busy condition of a lane / warp unit (its table is zero where it is free)
 __device__ __forceinline__ uint32_t own_bits(const P3Args &a, int u) {
     if (u == a.N) return 0u;
     if (u >= 2 && u <= 6) return 1u << (u - 2);
-    if (u >= 9 && u < 9 + a.nW) return 1u << (u - 9 + 5);
+    if (u >= 9 && u < 9 + a.nwv) return 1u << (u - 9 + 5);
     return 0u;
 }
 
 // Walk the trie for tile t, then sort the pairs by (unit, class, rm).
 // Returns the number of 16-byte records after the header, or -1 on overflow.
 __device__ int tile_program(const P3Args &a, uint32_t t, double *W0, PairAcc3 &P) {
-    const int NVU = 9 + a.nW;
+    const int NVU = 9 + a.nwv;
     uint32_t Sst[HQ_MAXN + 2];
     Sst[0] = 0;
     for (int u = 0; u <= HQ_MAXN; u++) W0[u] = 0.0;
@@ -857,7 +859,8 @@ __global__ void k_prog_write3(P3Args a, const uint32_t *__restrict__ order, cons
                               uint4 *__restrict__ prog, int *__restrict__ err) {
     PairAcc3 P;
     double W0[HQ_MAXN + 1];
-    const int NVU = 9 + a.nW;
+    const int NVU = 9 + a.nwv;      // units varying inside the program
+    const int NT = 9 + a.nW;        // first tile unit (mu_F: busy tile units only)
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.ntiles;
          i += (uint64_t)gridDim.x * blockDim.x) {
         uint4 *out = prog + off16[i];
@@ -918,7 +921,7 @@ __global__ void k_prog_write3(P3Args a, const uint32_t *__restrict__ order, cons
         double *w0o = reinterpret_cast<double *>(out + 8);
         for (int u = 0; u < 32; u++) w0o[u] = u <= HQ_MAXN ? W0[u] : 0.0;
         double muF = 0.0;
-        for (int u = NVU; u < a.N; u++)
+        for (int u = NT; u < a.N; u++)
             if ((t >> (u - NVU)) & 1u) muF += a.nu[u];
         uint32_t has = 0;
         for (int q = 0; q < 32; q++)

@@ -20,7 +20,7 @@
 #define V3_R 8                 // states per thread
 #define V3_MAXSLOTS 8          // CTA ring slots (one tile-sized block each)
 #define V3_HDR16 33            // program header: info[32] (u32), W0[32] (f64), {mu_F, has}, M[32] (u32)
-#define V3_MAXPAIRS 1024
+#define V3_MAXPAIRS 2048
 
 // program record of a warp tile (16-byte units):
 //   [0..7]   info[u] = n_lane | n_group << 8 | start << 16   (u = 0..N; N = blocked pseudo-unit)
@@ -43,8 +43,9 @@ struct S3Args {
     uint64_t chunk;          // tiles per CTA (contiguous range of the visit order)
     double Lam;
     double nu[32];           // internal-order service rates
-    const uint32_t *order;   // warp-tile visit order: entry i << nW | w = (t << nW) | w
-    const uint32_t *off16;   // program offset of warp-tile visit index (16-byte units)
+    const uint32_t *order;   // CTA-tile visit order (tile index t)
+    const uint32_t *off16;   // [ntiles << nW]: program of warp w of visit index i at off16[i << nW | w]
+                             // (CTA programs: the same offset for every warp of a tile)
     const uint4 *prog;
     uint32_t total16;
     uint32_t maxblk16;       // largest program block of a CTA tile (16-byte units)
@@ -60,9 +61,10 @@ struct S3Args {
     int full_lists;
 };
 
-struct P3Args {   // program precompute (per CTA tile)
+struct P3Args {   // program precompute (one program per warp tile or per CTA tile)
     int N;
-    int nW;
+    int nW;                  // log2(warps per CTA)
+    int nwv;                 // warp bits varying inside a program: nW (CTA programs) or 0 (warp programs)
     int full_lists;
     uint64_t ntiles;
     double nu[32];           // internal-order service rates (mu_F in the header)

@@ -1,1 +1,2 @@
-timeout 300 python tools/check_programs.py 19 40 0 2 > gpurun_out/chk.log 2>&1; echo rc=$?; tail -12 gpurun_out/chk.log
+CFG=3 VARIANTS="auto2 auto prev" bash tools/gpu_ab.sh
+CFG=4 REPS=2 VARIANTS="auto2 prev" bash tools/gpu_ab.sh
