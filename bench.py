@@ -121,15 +121,16 @@ def measured_peaks():
 
 
 def ncu_traffic(cfg):
-    """dram bytes (read + write) per sweep (gather + finalize launch pair) from the
-    committed ncu --set full summary, if one exists for this config."""
+    """DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) of one sweep-kernel launch
+    (k_sweep3, one half-sweep) from the committed `ncu --set full` capture of this config
+    (profiles/ncu_traffic.json, written by tools/ncu_traffic.py), or None."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(p):
         return None
     with open(p) as f:
         d = json.load(f)
     e = d.get(f"cfg{cfg}")
-    return None if e is None else e.get("dram_bytes_per_state_update")
+    return None if e is None else e.get("dram_bytes_per_launch")
 
 
 # ------------------------------------------------------------------ reference arm (CPU oracle)
@@ -149,13 +150,18 @@ def oracle_sample(inst, sweeps=3):
     return updates / dt, dt, oracle.num_threads()
 
 
+def cpu_sample_sweeps(N):
+    """Oracle sweeps per sample: about 10-20 s of CPU work on a 16-core host."""
+    return max(1, min(64, 16 << max(0, 24 - N)))
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return 0
     import hqinst
 
     inst = hqinst.config_instance(args.config, rho=args.rho)
-    sweeps = 1 if inst.N >= 26 else 2
+    sweeps = cpu_sample_sweeps(inst.N)
     for _ in range(args.warmup if inst.N <= 20 else 0):
         oracle_sample(inst, 1)
     vals = []
@@ -165,7 +171,8 @@ def run_reference(args, rank, world):
         vals.append(v)
         tt += dt
     value = statistics.median(vals)
-    sample = f"{sweeps} Algorithm-1 sweeps (+ per-sweep residual) of cfg{args.config} per step, rate-table build excluded"
+    sample = (f"{sweeps} Algorithm-1 sweeps of cfg{args.config} per step (each with the oracle's full residual pass), "
+              f"rate-table build excluded")
     line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * tt / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -293,21 +300,31 @@ def run_ours(args, rank, world, local_rank):
         return 0
 
     peak, peak_src = measured_peaks()
-    per_update_ms = sweep_ms / max(updates, 1.0)
-    achieved = BYTES_PER_UPDATE * updates / (sweep_ms * 1e-3) / 1e9 if sweep_ms > 0 else None
+    # dominant kernel: the sweep kernel (one launch per half-sweep), timed by CUDA events
+    # recorded around every launch on the solve stream inside hq_solve (hq_stats)
+    launch_ms = sweep_ms / max(sweep_launches, 1.0)
+    updates_per_launch = updates / max(sweep_launches, 1.0)
+    achieved = BYTES_PER_UPDATE * updates_per_launch / (launch_ms * 1e-3) / 1e9 if sweep_ms > 0 else None
     traffic = ncu_traffic(args.config)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None,
-                "traffic": traffic, "traffic_unit": "dram bytes per state update (ncu --set full)" if traffic else None,
-                "kernel": "sweep = k_gather + k_layer_reduce + k_finalize per half-sweep (CUDA events on the solve stream)",
-                "algorithmic_bytes_per_state_update": BYTES_PER_UPDATE, "peak_source": peak_src,
+                "traffic": traffic,
+                "traffic_note": "DRAM bytes per k_sweep3 launch from ncu --set full (profiles/ncu_traffic.json)"
+                if traffic else None,
+                "kernel": "k_sweep3 (one launch per half-sweep of the red-black schedule)",
+                "algorithmic_bytes_per_state_update": BYTES_PER_UPDATE,
+                "algorithmic_bytes_per_launch": BYTES_PER_UPDATE * updates_per_launch,
+                "launch_ms": launch_ms, "launches_per_step": sweep_launches / args.steps,
+                "peak_source": peak_src,
                 "sweep_ms_per_step": sweep_ms / args.steps, "sweep_share_of_step": sweep_ms / ms if ms else None}
     line = {"metric": METRIC, "value": updates_tot / (ms_max * 1e-3), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded EMS-shaped instance, hqinst)",
             "config": dict(workload_desc(inst, args.config), tol=args.tol,
-                           l2="working set (pi + p + (a,b) scratch) = %.0f MB vs 126 MB L2" % (3 * 8 * (1 << inst.N) / 2 ** 20),
+                           l2="inputs larger than L2: per half-sweep the kernel streams %.0f MB (both classes of p, "
+                              "omega/kappa, rate programs) vs 126 MB L2; no explicit flush"
+                              % ((8 + 8 + 16) * (1 << inst.N) / 2 / 2 ** 20),
                            parallelism="replicas" if world > 1 else "single GPU"),
             "time_to_tol_ms": statistics.median(solve_ms), "sweeps": statistics.median(iters),
             "residual": max(res), "roofline": roofline, "gpu_launches": int(launches),
@@ -316,10 +333,11 @@ def run_ours(args, rank, world, local_rank):
         line["clocks"] = ck
     if not args.no_cpu_baseline and world == 1:
         try:
-            v, dt, cores = oracle_sample(inst, 1 if inst.N >= 26 else 2)
+            ns = cpu_sample_sweeps(inst.N)
+            v, dt, cores = oracle_sample(inst, ns)
             line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
-                                    "sample": f"{1 if inst.N >= 26 else 2} Algorithm-1 sweeps of cfg{args.config} "
-                                              f"(+ per-sweep residual), rate-table build excluded, {dt:.1f} s"}
+                                    "sample": f"{ns} Algorithm-1 sweeps of cfg{args.config} (each with the oracle's "
+                                              f"full residual pass), rate-table build excluded, {dt:.1f} s"}
         except Exception as ex:  # the oracle is a reported baseline, never the product
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": None, "kind": "oracle",
                                     "sample": f"failed: {ex}"}
