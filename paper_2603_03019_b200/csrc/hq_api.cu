@@ -1075,6 +1075,7 @@ static cudaError_t tiled_sweep(hq_problem *h, const S2Args &sa, int mode, cudaSt
     a.blk = h->d_blk;
     a.done = h->d_done;
     a.full_lists = sa.full_lists;
+    a.warp_programs = (h->prog_nwv == 0) ? 1 : 0;
     a.Q = sa.Q;
     a.P = sa.P;
     a.omkap = sa.omkap;

@@ -170,27 +170,30 @@ __device__ __forceinline__ uint32_t ldpu(const uint32_t *p, uint64_t pol) {
 // pext(l, M & 31) | pext(w, M >> 5) << popc(M & 31), from two small shared tables.  The
 // block is staged in shared memory with the tile's q block (generic pointer: an oversized
 // block stays in global memory).
+template <bool WP>   // WP: warp-tile programs (tables indexed by lane bits only)
 struct Prog {
-    const uint4 *pg;        // header
+    const uint4 *pg;        // header: pg[u] = {info, M, W0 lo, W0 hi}; pg[32] = {mu_F lo, hi, has, 0}
     const uint8_t *pl;      // pl[M5 * 32] = pext(lane, M5) for this lane (stride 32)
     const uint8_t *pw;      // pw[M4 * 16] = pext(warp, M4) for this warp (stride 16)
-    uint32_t info;          // info[lane]: (table << 31) | start << 8 | ngroups
-    uint32_t infm;          // M of the table of unit `lane`
-    double w0;              // W0[lane]
-    __device__ __forceinline__ double W0(int u) const { return __shfl_sync(0xffffffffu, w0, u); }
+    __device__ __forceinline__ uint4 hdr(int u) const { return pg[u]; }
     __device__ __forceinline__ uint32_t idx(uint32_t M) const {
+        if (WP) return pl[M * 32];
         return (uint32_t)pl[(M & 31u) * 32] | ((uint32_t)pw[(M >> 5) * 16] << __popc(M & 31u));
     }
 };
-__device__ __forceinline__ double unit_rates(const Prog &P, int u, int lane, int sh, double w0,
+__device__ __forceinline__ double hdr_w0(const uint4 &h) { return __hiloint2double((int)h.w, (int)h.z); }
+
+// rate of unit u for this thread (w0: the tile-uniform part, already masked by the caller
+// for a lane unit that is free in this lane); register-dependent groups go to A directly
+template <bool WP>
+__device__ __forceinline__ double unit_rates(const Prog<WP> &P, const uint4 &h, int sh, double w0,
                                              const double (&q)[R], double (&A)[R]) {
-    (void)lane;
-    const uint32_t inf = __shfl_sync(0xffffffffu, P.info, u);
-    const uint32_t Mt = __shfl_sync(0xffffffffu, P.infm, u);
+    const uint32_t inf = h.x;
     if (!inf) return w0;
     const uint4 *d = P.pg + V3_HDR16 + ((inf >> 8) & 0xffffu);
     double Wt = w0;
     if (inf >> 31) {
+        const uint32_t Mt = h.y;
         Wt = reinterpret_cast<const double *>(d)[P.idx(Mt)];
         d += ((1 << __popc(Mt)) + 1) >> 1;
     }
@@ -240,7 +243,7 @@ __device__ __forceinline__ double2 ldg_ef(const double2 *p) {
 
 
 
-template <int MODE, bool FULL>
+template <int MODE, bool FULL, bool WP>
 __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
     using SL = Slots<MODE, FULL>;
     constexpr int NB = SL::NB;
@@ -397,7 +400,7 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
             load_tile(k + 1);
         }
         const double *tq = tileq + (size_t)buf * BUFD;
-        Prog P;
+        Prog<WP> P;
         {
             const uint64_t widx = (uint64_t)tidx << nW;
             const uint32_t o0 = __ldg(a.off16 + widx), ow = __ldg(a.off16 + widx + warp);
@@ -405,9 +408,6 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
             P.pg = nrec <= a.maxblk16 ? reinterpret_cast<const uint4 *>(tq + TS) + (ow - o0) : a.prog + ow;
             P.pl = s_pext + lane;
             P.pw = s_pextw + warp;
-            P.info = reinterpret_cast<const uint32_t *>(P.pg)[lane];
-            P.infm = reinterpret_cast<const uint32_t *>(P.pg + 25)[lane];
-            P.w0 = reinterpret_cast<const double *>(P.pg + 8)[lane];
         }
         const int K = __popc(t);
         if (K != curK) {
@@ -416,7 +416,7 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
         }
         const int beta = a.c ^ (K & 1) ^ par_t;
         const int sh = beta ? 8 : 0;
-        const double mu_F = reinterpret_cast<const double *>(P.pg + 24)[0];
+        const double mu_F = reinterpret_cast<const double *>(P.pg + 32)[0];
 
         double qo[R], A[R], D[R], q[R];
 #pragma unroll
@@ -432,7 +432,8 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
         }
         // ---- unit 0 (implied parity bit): busy in r iff b0(r) = beta ^ parity(r)
         {
-            const double Wt = unit_rates(P, 0, lane, sh, P.W0(0), qo, A);
+            const uint4 h0 = P.hdr(0);
+            const double Wt = unit_rates(P, h0, sh, hdr_w0(h0), qo, A);
             const double We = beta ? Wt : 0.0, Wo = beta ? 0.0 : Wt;
             const double Ne = beta ? 0.0 : nu0, No = beta ? nu0 : 0.0;
 #pragma unroll
@@ -449,7 +450,8 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
             const int bit = 1 << rb;
 #pragma unroll
             for (int r = 0; r < R; r++) q[r] = qo[r ^ bit];
-            const double Wt = unit_rates(P, u, lane, sh, P.W0(u), q, A);
+            const uint4 hu = P.hdr(u);
+            const double Wt = unit_rates(P, hu, sh, hdr_w0(hu), q, A);
             const double nuu = a.nu[u];
 #pragma unroll
             for (int r = 0; r < R; r++) {
@@ -469,8 +471,8 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
                 q[2 * kk] = v.x;
                 q[2 * kk + 1] = v.y;
             }
-            const double w0u = P.W0(u);   // warp-wide shuffle: outside the lane-dependent select
-            const double Wt = unit_rates(P, u, lane, sh, busy ? w0u : 0.0, q, A);
+            const uint4 hu = P.hdr(u);
+            const double Wt = unit_rates(P, hu, sh, busy ? hdr_w0(hu) : 0.0, q, A);
             const double wn = busy ? 0.0 : a.nu[u];
 #pragma unroll
             for (int r = 0; r < R; r++) {
@@ -489,7 +491,8 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
                 q[2 * kk + 1] = v.y;
             }
             if ((warp >> b) & 1) {
-                const double Wt = unit_rates(P, u, lane, sh, P.W0(u), q, A);
+                const uint4 hu = P.hdr(u);
+                const double Wt = unit_rates(P, hu, sh, hdr_w0(hu), q, A);
 #pragma unroll
                 for (int r = 0; r < R; r++) A[r] = fma(Wt, q[r], A[r]);
             } else {
@@ -498,22 +501,23 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
                 for (int r = 0; r < R; r++) D[r] = fma(nuu, q[r], D[r]);
             }
         }
-        // ---- tile units (H): neighbour tile slices straight from global memory (L2)
-        for (int h = 0; h < nH; h++) {
+        // ---- tile units (H): neighbour tile slices straight from global memory (L2), two
+        //      units of loads in flight; unrolled by two so the buffers alternate in place
+        auto unit_H = [&](int h, double2 (&buf)[4]) {
             const int u = NVU + h;
 #pragma unroll
             for (int kk = 0; kk < 4; kk++) {
-                q[2 * kk] = pa[kk].x;
-                q[2 * kk + 1] = pa[kk].y;
-                pa[kk] = pb2[kk];
+                q[2 * kk] = buf[kk].x;
+                q[2 * kk + 1] = buf[kk].y;
             }
             if (h + 2 < nH) {
                 const double *src = hsrc(h + 2);
 #pragma unroll
-                for (int kk = 0; kk < 4; kk++) pb2[kk] = ldg2(src + (kk << 6), pol_el);
+                for (int kk = 0; kk < 4; kk++) buf[kk] = ldg2(src + (kk << 6), pol_el);
             }
             if ((t >> h) & 1u) {
-                const double Wt = unit_rates(P, u, lane, sh, P.W0(u), q, A);
+                const uint4 hu = P.hdr(u);
+                const double Wt = unit_rates(P, hu, sh, hdr_w0(hu), q, A);
 #pragma unroll
                 for (int r = 0; r < R; r++) A[r] = fma(Wt, q[r], A[r]);
             } else {
@@ -521,6 +525,10 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
 #pragma unroll
                 for (int r = 0; r < R; r++) D[r] = fma(nuu, q[r], D[r]);
             }
+        };
+        for (int h = 0; h < nH; h += 2) {
+            unit_H(h, pa);
+            if (h + 1 < nH) unit_H(h + 1, pb2);
         }
         // ---- lambda_m: Lambda minus the atoms whose whole (truncated) list is busy
         double lam[R];
@@ -534,7 +542,8 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
                 lam[r] = 0.0;
                 one[r] = 1.0;
             }
-            const double Bt = unit_rates(P, a.N, lane, sh, P.W0(a.N), one, lam);
+            const uint4 hN = P.hdr(a.N);
+            const double Bt = unit_rates(P, hN, sh, hdr_w0(hN), one, lam);
 #pragma unroll
             for (int r = 0; r < R; r++) lam[r] = a.Lam - (lam[r] + Bt);
         }
@@ -915,18 +924,18 @@ __global__ void k_prog_write3(P3Args a, const uint32_t *__restrict__ order, cons
             if (ng > 255 || start > 0xffffu) atomicExch(err, 3);
             info[u] = inf | ng | (start << 8);
         }
-        for (int q = 0; q < 8; q++) out[q] = make_uint4(info[4 * q], info[4 * q + 1], info[4 * q + 2], info[4 * q + 3]);
-        for (int q = 0; q < 8; q++)
-            out[25 + q] = make_uint4(infm[4 * q], infm[4 * q + 1], infm[4 * q + 2], infm[4 * q + 3]);
-        double *w0o = reinterpret_cast<double *>(out + 8);
-        for (int u = 0; u < 32; u++) w0o[u] = u <= HQ_MAXN ? W0[u] : 0.0;
+        for (int u = 0; u < 32; u++) {
+            const double w = u <= HQ_MAXN ? W0[u] : 0.0;
+            out[u] = make_uint4(info[u], infm[u], (uint32_t)__double_as_longlong(w),
+                                (uint32_t)((unsigned long long)__double_as_longlong(w) >> 32));
+        }
         double muF = 0.0;
         for (int u = NT; u < a.N; u++)
             if ((t >> (u - NVU)) & 1u) muF += a.nu[u];
         uint32_t has = 0;
         for (int q = 0; q < 32; q++)
             if (info[q]) has |= 1u << q;
-        out[24] = make_uint4((uint32_t)__double_as_longlong(muF),
+        out[32] = make_uint4((uint32_t)__double_as_longlong(muF),
                              (uint32_t)((unsigned long long)__double_as_longlong(muF) >> 32), has, 0u);
     }
 }
@@ -974,28 +983,33 @@ cudaError_t prog_write(const P3Args &a, const uint32_t *order, const uint32_t *o
     return cudaGetLastError();
 }
 
-template <int MODE, bool FULL>
+template <int MODE, bool FULL, bool WP>
 static cudaError_t launch(const S3Args &a, int grid, cudaStream_t s) {
     const size_t sm = sweep_smem(a.nW, a.maxblk16, a.nslots);
-    cudaError_t e = cudaFuncSetAttribute(hq3::k_sweep3<MODE, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaError_t e = cudaFuncSetAttribute(hq3::k_sweep3<MODE, FULL, WP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
-    // leave the rest of the unified L1/shared array to L1 (rate programs are read through it)
+    // leave the rest of the unified L1/shared array to L1
     const int carve = (int)std::min<size_t>(100, (sm + 2048) * 100 / (228 * 1024) + 1);
-    e = cudaFuncSetAttribute(hq3::k_sweep3<MODE, FULL>, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
+    e = cudaFuncSetAttribute(hq3::k_sweep3<MODE, FULL, WP>, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
     if (e != cudaSuccess) return e;
-    hq3::k_sweep3<MODE, FULL><<<grid, 32 << a.nW, sm, s>>>(a);
+    hq3::k_sweep3<MODE, FULL, WP><<<grid, 32 << a.nW, sm, s>>>(a);
     return cudaGetLastError();
 }
 
-cudaError_t sweep(const S3Args &a, int full, int mode, int grid, cudaStream_t s) {
+template <bool WP>
+static cudaError_t sweep_wp(const S3Args &a, int full, int mode, int grid, cudaStream_t s) {
     if (full) {
-        if (mode == 0) return launch<0, true>(a, grid, s);
-        if (mode == 1) return launch<1, true>(a, grid, s);
-        return launch<2, true>(a, grid, s);
+        if (mode == 0) return launch<0, true, WP>(a, grid, s);
+        if (mode == 1) return launch<1, true, WP>(a, grid, s);
+        return launch<2, true, WP>(a, grid, s);
     }
-    if (mode == 0) return launch<0, false>(a, grid, s);
-    if (mode == 1) return launch<1, false>(a, grid, s);
-    return launch<2, false>(a, grid, s);
+    if (mode == 0) return launch<0, false, WP>(a, grid, s);
+    if (mode == 1) return launch<1, false, WP>(a, grid, s);
+    return launch<2, false, WP>(a, grid, s);
+}
+
+cudaError_t sweep(const S3Args &a, int full, int mode, int grid, cudaStream_t s) {
+    return a.warp_programs ? sweep_wp<true>(a, full, mode, grid, s) : sweep_wp<false>(a, full, mode, grid, s);
 }
 
 }  // namespace hq3_launch

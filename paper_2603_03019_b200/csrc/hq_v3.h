@@ -19,20 +19,20 @@
 
 #define V3_R 8                 // states per thread
 #define V3_MAXSLOTS 8          // CTA ring slots (one tile-sized block each)
-#define V3_HDR16 33            // program header: info[32] (u32), W0[32] (f64), {mu_F, has}, M[32] (u32)
+#define V3_HDR16 33            // program header: {info, M, W0} x 32 units, {mu_F, has}
 #define V3_MAXPAIRS 2048
 
-// program record of a warp tile (16-byte units):
-//   [0..7]   info[u] = n_lane | n_group << 8 | start << 16   (u = 0..N; N = blocked pseudo-unit)
-//   [8..23]  W0[u] (f64): warp-tile-uniform rate part of unit u
-//   [24]     {mu_F (f64), has, 0}: mu_F = sum of nu over the busy units >= 9;
-//            has = bit u set iff unit u has pairs (info[u] != 0)
-//   records  per unit: n_lane lane-only pairs {c.lo, c.hi, S_t, 0}, then n_group groups,
-//            each a header {0, 0, count, rm} followed by count pairs {c.lo, c.hi, S_t, 0}.
-//            S_t = unit bits of the lane units that must be busy (thread-level
-//            condition); rm = admissible register states for beta = 0 (bits 0..7) and
-//            beta = 1 (bits 8..15) of every pair of the group.
-// The programs of the 2^nW warp tiles of a CTA tile are stored contiguously.
+// rate program of a warp tile or of a CTA tile (16-byte records):
+//   [0..31]  per unit u (u = N: blocked pseudo-unit): {info, M, W0 lo, W0 hi}
+//            info = table << 31 | start << 8 | n_group (0: no data, W0 alone applies);
+//            M = thread bits the unit's table is indexed by (lane bits 0..4, warp bits 5..8);
+//            W0 = the tile-uniform rate of the unit
+//   [32]     {mu_F lo, mu_F hi, has, 0}: mu_F = sum of nu over the busy tile units
+//   data     per unit with data, at record 33 + start: a table of 2^|M| fp64 entries (if
+//            info >> 31), then n_group groups, each a header {rm | M_g << 16, 0, 0, 0} and a
+//            table of 2^|M_g| entries; rm = admissible register states for beta = 0
+//            (bits 0..7) and beta = 1 (bits 8..15).  A thread's entry is pext(thread bits, M).
+// The programs of the warp tiles of a CTA tile (or its one CTA program) are contiguous.
 
 struct S3Args {
     int N;
@@ -59,6 +59,7 @@ struct S3Args {
     double *blk;             // the scalar block, updated by the last CTA (MODE 0/1)
     unsigned *done;          // CTA completion counter (self-resetting)
     int full_lists;
+    int warp_programs;       // 1: one rate program per warp tile (tables over lane bits only)
 };
 
 struct P3Args {   // program precompute (one program per warp tile or per CTA tile)

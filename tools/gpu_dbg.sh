@@ -1,2 +1,3 @@
-CFG=3 VARIANTS="auto2 auto prev" bash tools/gpu_ab.sh
-CFG=4 REPS=2 VARIANTS="auto2 prev" bash tools/gpu_ab.sh
+timeout 300 python -m pytest tests/test_gpu_parity.py -q -x -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?; tail -2 gpurun_out/pytest_gpu.log
+CFG=3 VARIANTS="hdr auto" bash tools/gpu_ab.sh
+CFG=4 REPS=2 VARIANTS="hdr auto" bash tools/gpu_ab.sh
