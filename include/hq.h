@@ -135,9 +135,11 @@ const char *hq_error_string(hq_handle h);
  *   rate programs, [13] code path (1: N < 8 two-pass, 2: warp-tiled, 3: CTA-tiled),
  *   [14] largest rate-program block of a CTA tile (16-byte records),
  *   [15] warp bits varying inside a rate program (0: one program per warp tile,
- *        nW: one program per CTA tile; chosen by timing both at the first solve).
+ *        nW: one program per CTA tile; chosen by timing both at the first solve),
+ *   [16], [17] timed sweep launches (ms) with CTA / warp programs at that choice
+ *        (0: not timed).
  */
-#define HQ_STATS_LEN 16
+#define HQ_STATS_LEN 20
 hq_status hq_stats(hq_handle h, double *out);
 
 /* Copy an internal device array to host memory (tests and debugging only):

@@ -309,6 +309,7 @@ struct hq_problem {
     int nslots = 0;                // path 3: CTA ring slots
     uint32_t maxblk_all = 0;       // path 3: largest program block of a CTA tile (records)
     unsigned *d_done = nullptr;    // path 3: CTA completion counter of the fused scalar step
+    unsigned long long *d_wtime = nullptr;   // path 3: per-warp busy cycles (-DHQ_WARP_TIMING builds)
     int prog_nwv = 0;              // path 3: warp bits varying inside a rate program (nW: CTA programs)
     float tune_ms[2] = {0.f, 0.f}; // path 3: timed sweeps with CTA / warp programs (0: not tuned)
     uint32_t *d_order = nullptr, *d_off16 = nullptr, *d_size16 = nullptr, *d_range = nullptr;
@@ -350,6 +351,8 @@ struct hq_problem {
         d_range = nullptr;
         cudaFree(d_done);
         d_done = nullptr;
+        cudaFree(d_wtime);
+        d_wtime = nullptr;
         cudaFree(d_off16);
         cudaFree(d_size16);
         cudaFree(d_prog);
@@ -859,16 +862,21 @@ static hq_status v3_programs(hq_problem *h, cudaStream_t s, int nwv, const std::
     double tot = 0.0;
     ps.maxblk = 0;
     for (uint64_t i = 0; i < ntiles; i++) {
-        uint32_t b = 0;
+        uint32_t b = 0, bmax = 0;
         for (uint64_t w = 0; w < W; w++) {
             off16[(i << nW) | w] = per_warp ? offp[(i << nW) | w] : offp[i];
-            if (per_warp) b += sz[(i << nW) | w];
+            if (per_warp) {
+                b += sz[(i << nW) | w];
+                bmax = std::max(bmax, sz[(i << nW) | w]);
+            }
         }
-        if (!per_warp) b = sz[i];
+        if (!per_warp) b = bmax = sz[i];
         ps.maxblk = std::max(ps.maxblk, b);
         // estimated work of a tile in program-record units: the gather of its states plus
-        // the evaluation of the program records (every warp evaluates a CTA program)
+        // the evaluation of the program records (every warp evaluates a CTA program).  Chosen
+        // by same-box A/B timing; models fitted to per-warp busy cycles balanced worse.
         cost[i] = 256.0 + (double)b * (per_warp ? 1.0 : (double)W / 4.0);
+        (void)bmax;
         tot += cost[i];
     }
     HQ_CUDA(cudaMemcpyAsync(ps.off16, off16.data(), 4 * off16.size(), cudaMemcpyHostToDevice, s));
@@ -1076,6 +1084,8 @@ static cudaError_t tiled_sweep(hq_problem *h, const S2Args &sa, int mode, cudaSt
     a.done = h->d_done;
     a.full_lists = sa.full_lists;
     a.warp_programs = (h->prog_nwv == 0) ? 1 : 0;
+    if (!h->d_wtime && cudaMalloc((void **)&h->d_wtime, 8 * 4096) == cudaSuccess) cudaMemset(h->d_wtime, 0, 8 * 4096);
+    a.wtime = h->d_wtime;
     a.Q = sa.Q;
     a.P = sa.P;
     a.omkap = sa.omkap;
@@ -1298,6 +1308,8 @@ extern "C" hq_status hq_solve(hq_handle h, double tol, int max_iter, double *pi,
         h->stats[13] = h->path;   // path id
         h->stats[14] = h->maxblk_all;
         h->stats[15] = h->prog_nwv;
+        h->stats[16] = h->tune_ms[0];
+        h->stats[17] = h->tune_ms[1];
         if (iters_out) *iters_out = o.sweeps;
         if (residual_out) *residual_out = o.res;
         if (!std::isfinite(o.res)) {
@@ -1504,6 +1516,8 @@ extern "C" hq_status hq_debug_copy(hq_handle h, int which, void *host, size_t by
         case 3: src = h->d_prog; break;
         case 4: src = h->d_off16; break;
         case 5: src = h->d_order; break;
+        case 7: src = h->d_wtime; break;
+        case 8: src = h->d_range; break;
         default: return HQ_E_INVAL;
     }
     if (!src) return HQ_E_ORDER;

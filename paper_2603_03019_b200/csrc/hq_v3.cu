@@ -399,6 +399,9 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
             fence_proxy_async();
             load_tile(k + 1);
         }
+#ifdef HQ_WARP_TIMING
+        const long long tw0 = clock64();
+#endif
         const double *tq = tileq + (size_t)buf * BUFD;
         Prog<WP> P;
         {
@@ -605,6 +608,10 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
         for (int h = 0; h < 3; h++)
 #pragma unroll
             for (int v = 0; v < NB; v++) sb[(h * NB + v) * nthr + tid] += bins[h][v];
+#ifdef HQ_WARP_TIMING
+        if (lane == 0 && MODE == 0)
+            atomicAdd(a.wtime + (blockIdx.x << nW) + warp, (unsigned long long)(clock64() - tw0));
+#endif
         if (MODE < 2) {
 #pragma unroll
             for (int kk = 0; kk < 4; kk++) {

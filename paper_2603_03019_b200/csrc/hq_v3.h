@@ -60,6 +60,7 @@ struct S3Args {
     unsigned *done;          // CTA completion counter (self-resetting)
     int full_lists;
     int warp_programs;       // 1: one rate program per warp tile (tables over lane bits only)
+    unsigned long long *wtime;   // -DHQ_WARP_TIMING builds: busy cycles per (CTA, warp)
 };
 
 struct P3Args {   // program precompute (one program per warp tile or per CTA tile)

@@ -21,7 +21,7 @@ HQ_E_NOMEM = -2
 HQ_E_CUDA = -3
 HQ_E_NUMERIC = -4
 HQ_E_ORDER = -5
-HQ_STATS_LEN = 16
+HQ_STATS_LEN = 20
 STATUS_NAMES = {0: "HQ_OK", 1: "HQ_NOT_CONVERGED", -1: "HQ_E_INVAL", -2: "HQ_E_NOMEM", -3: "HQ_E_CUDA",
                 -4: "HQ_E_NUMERIC", -5: "HQ_E_ORDER"}
 EXPORTED = ["hq_create", "hq_solve", "hq_measures", "hq_destroy", "hq_error_string", "hq_stats", "hq_version",
@@ -190,7 +190,7 @@ class Solver:
         s = hq_stats(self.h)
         keys = ["sweeps", "halfsweeps", "state_updates", "launches", "residual_evals", "trie_nodes", "sum_pi_minus_1",
                 "solve_ms", "sweep_ms", "sweep_launches", "residual_ms", "precompute_ms", "program_bytes", "path",
-                "max_program_block", "program_nwv"]
+                "max_program_block", "program_nwv", "tune_ms_cta", "tune_ms_warp"]
         return {k: float(s[i]) for i, k in enumerate(keys)}
 
     def close(self):

@@ -37,13 +37,17 @@ out = []
 for _ in range(int(os.environ["REPS"])):
     r = s.solve(tol=1e-13, max_iter=5000, pi=pi)
     st = s.stats()
-    out.append((st["solve_ms"], st["sweep_ms"], r["iters"], r["residual"]))
+    out.append((st["solve_ms"], st["sweep_ms"], r["iters"], r["residual"], st.get("program_nwv", -1),
+                st.get("tune_ms_cta", 0), st.get("tune_ms_warp", 0)))
 print(json.dumps(out))
 '''
 res = {n: [] for n in names}
 for rnd in range(2):   # two interleaved rounds of fresh processes
     for n in names:
-        env = dict(os.environ, ROOT=ROOT, CFG=str(cfg), REPS=str(reps), HQ_LIB=os.path.join(VAR, f"libhq_{n}.so"))
+        lib, _, prog = n.partition("@")   # NAME@cta / NAME@warp forces the program granularity
+        env = dict(os.environ, ROOT=ROOT, CFG=str(cfg), REPS=str(reps), HQ_LIB=os.path.join(VAR, f"libhq_{lib}.so"))
+        if prog:
+            env["HQ_PROG"] = prog
         p = subprocess.run([sys.executable, "-c", child], env=env, capture_output=True, text=True, timeout=600)
         if p.returncode != 0:
             print(n, "FAILED", p.stderr[-2000:])
@@ -54,5 +58,7 @@ for n in names:
         continue
     solve = statistics.median(x[0] for x in res[n])
     sweep = statistics.median(x[1] for x in res[n])
-    print(json.dumps(dict(variant=n, solve_ms=round(solve, 2), sweep_ms=round(sweep, 2), iters=res[n][0][2],
-                          residual=res[n][0][3], samples=len(res[n]))))
+    x = res[n][0]
+    print(json.dumps(dict(variant=n, solve_ms=round(solve, 2), sweep_ms=round(sweep, 2), iters=x[2],
+                          residual=x[3], samples=len(res[n]), prog_nwv=x[4] if len(x) > 4 else None,
+                          tune_ms=(x[5], x[6]) if len(x) > 6 else None)))
