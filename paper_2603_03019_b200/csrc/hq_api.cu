@@ -880,15 +880,35 @@ static hq_status v3_programs(hq_problem *h, cudaStream_t s, int nwv, const std::
         tot += cost[i];
     }
     HQ_CUDA(cudaMemcpyAsync(ps.off16, off16.data(), 4 * off16.size(), cudaMemcpyHostToDevice, s));
+    // optimal contiguous partition into G ranges (minimise the largest range cost): binary
+    // search on the bottleneck with greedy packing
     const int G = h->sgrid;
     std::vector<uint32_t> range(G + 1, (uint32_t)ntiles);
-    range[0] = 0;
-    double acc = 0.0;
-    int b = 1;
-    for (uint64_t i = 0; i < ntiles && b < G; i++) {
-        acc += cost[i];
-        while (b < G && acc >= tot * b / G) range[b++] = (uint32_t)(i + 1);
+    auto pack = [&](double cap, std::vector<uint32_t> *out) -> bool {
+        int b = 0;
+        double acc = 0.0;
+        if (out) (*out)[0] = 0;
+        for (uint64_t i = 0; i < ntiles; i++) {
+            if (cost[i] > cap) return false;
+            if (acc + cost[i] > cap) {
+                if (++b >= G) return false;
+                if (out) (*out)[b] = (uint32_t)i;
+                acc = 0.0;
+            }
+            acc += cost[i];
+        }
+        if (out)
+            for (int q = b + 1; q <= G; q++) (*out)[q] = (uint32_t)ntiles;
+        return true;
+    };
+    double lo = tot / G, hi = tot;
+    for (uint64_t i = 0; i < ntiles; i++) lo = std::max(lo, cost[i]);
+    for (int it = 0; it < 60 && hi - lo > 1e-9 * hi; it++) {
+        const double mid = 0.5 * (lo + hi);
+        if (pack(mid, nullptr)) hi = mid;
+        else lo = mid;
     }
+    pack(hi, &range);
     HQ_CUDA(cudaMalloc((void **)&ps.range, 4 * (G + 1)));
     HQ_CUDA(cudaMemcpyAsync(ps.range, range.data(), 4 * (G + 1), cudaMemcpyHostToDevice, s));
     HQ_CUDA(cudaMemcpyAsync(&herr, h->d_err, sizeof(int), cudaMemcpyDeviceToHost, s));
