@@ -505,7 +505,7 @@ static hq_status ensure_device(hq_problem *h) {
     HQ_CUDA(alloc((void **)&h->d_lam, sizeof(double) * h->J));
     HQ_CUDA(alloc((void **)&h->d_pref, sizeof(int32_t) * h->J * N));
     HQ_CUDA(alloc((void **)&h->d_partial, sizeof(double) * 2 * std::max(h->grid, h->sgrid) * HQ_NL * HQ_NV));
-    HQ_CUDA(alloc((void **)&h->d_blk, sizeof(double) * V2S_TOTAL));
+    HQ_CUDA(alloc((void **)&h->d_blk, sizeof(double) * 2 * V2S_TOTAL));   // [0]: the block, [1]: fold buffer
     HQ_CUDA(cudaMallocHost((void **)&h->h_blk, sizeof(double) * V2S_TOTAL));
     HQ_CUDA(alloc((void **)&h->d_small, sizeof(double) * S_TOTAL));
     HQ_CUDA(alloc((void **)&h->d_err, sizeof(int)));
@@ -939,7 +939,17 @@ static void use_progset(hq_problem *h, ProgSet &ps) {
     ps.prog = nullptr;
 }
 
-static cudaError_t tiled_sweep(hq_problem *h, const S2Args &sa, int mode, cudaStream_t s);
+// folded scalar step of a path-3 sweep launch (S3Args::fold)
+struct FoldArgs {
+    int fold = 0;
+    int prev_c = 0;
+    uint32_t prev_active = 0;
+    const double *prev_partial = nullptr;
+    double *blk_out = nullptr;
+};
+
+static cudaError_t tiled_sweep(hq_problem *h, const S2Args &sa, int mode, cudaStream_t s,
+                               const FoldArgs *f = nullptr);
 static S2Args base_s2(hq_problem *h);
 
 // time MODE-0 sweep launches with the programs now installed (the iterate is garbage:
@@ -1006,17 +1016,18 @@ static hq_status v3_prepare(hq_problem *h, cudaStream_t s) {
         HQ_CUDA(cudaMalloc((void **)&h->d_done, sizeof(unsigned)));
         HQ_CUDA(cudaMemsetAsync(h->d_done, 0, sizeof(unsigned), s));
     }
-    // program granularity: CTA programs (warps share one program; balanced) or warp
-    // programs (warp bits folded; fewer pairs per thread).  HQ_PROG=cta|warp forces one;
-    // otherwise both are built and the faster sweep is kept.
+    // program granularity: warp programs (warp bits folded; fewer pairs per thread; the
+    // default) or CTA programs (warps share one program).  HQ_PROG=cta forces CTA programs;
+    // HQ_PROG=auto builds both and keeps the faster sweep (timing-dependent, so results may
+    // differ bitwise between handles -- development only; the default is deterministic).
     const char *env = getenv("HQ_PROG");
-    const std::string pref = env ? env : "";
+    const std::string pref = env ? env : "warp";
     ProgSet a, b;
     hq_status st;
-    if (pref == "warp" || h->nW == 0) {
+    if (pref != "cta" && pref != "auto") {
         st = v3_programs(h, s, 0, order, a);
         if (st != HQ_OK) return st;
-    } else if (pref == "cta") {
+    } else if (pref == "cta" || h->nW == 0) {
         st = v3_programs(h, s, h->nW, order, a);
         if (st != HQ_OK) return st;
     } else {
@@ -1081,7 +1092,7 @@ static hq_status v3_prepare(hq_problem *h, cudaStream_t s) {
 }
 
 // one sweep / residual launch of the tiled paths (2: hq_v2.cu, 3: hq_v3.cu)
-static cudaError_t tiled_sweep(hq_problem *h, const S2Args &sa, int mode, cudaStream_t s) {
+static cudaError_t tiled_sweep(hq_problem *h, const S2Args &sa, int mode, cudaStream_t s, const FoldArgs *f) {
     if (h->path != 3) return hq2_launch::sweep(sa, mode, h->sgrid, s);
     S3Args a;
     memset(&a, 0, sizeof(a));
@@ -1104,6 +1115,7 @@ static cudaError_t tiled_sweep(hq_problem *h, const S2Args &sa, int mode, cudaSt
     a.done = h->d_done;
     a.full_lists = sa.full_lists;
     a.warp_programs = (h->prog_nwv == 0) ? 1 : 0;
+    a.all_staged = h->maxblk_all <= h->maxrec ? 1 : 0;
     if (!h->d_wtime && cudaMalloc((void **)&h->d_wtime, 8 * 4096) == cudaSuccess) cudaMemset(h->d_wtime, 0, 8 * 4096);
     a.wtime = h->d_wtime;
     a.Q = sa.Q;
@@ -1111,6 +1123,13 @@ static cudaError_t tiled_sweep(hq_problem *h, const S2Args &sa, int mode, cudaSt
     a.omkap = sa.omkap;
     a.coef = sa.coef;
     a.partial = sa.partial;
+    if (f && f->fold) {
+        a.fold = 1;
+        a.prev_c = f->prev_c;
+        a.prev_active = f->prev_active;
+        a.prev_partial = f->prev_partial;
+        a.blk_out = f->blk_out;
+    }
     return hq3_launch::sweep(a, sa.full_lists, mode, h->sgrid, s);
 }
 
@@ -1192,6 +1211,27 @@ static hq_status solve_v2(hq_problem *h, double tol, int max_iter, double *pi, c
 
     S2Args sa = base_s2(h);
 
+    // path 3 folds the scalar step of half-sweep t into the prologue of launch t + 1
+    // (S3Args::fold): the scalar block and the CTA partials are double-buffered; a pending
+    // step is resolved by k_scalars2 before the host reads the block or a residual runs.
+    // (only where the per-CTA partial reduction is short: <= 48 loads per thread)
+    const bool fold = h->path == 3 && !hq3_launch::fused_scalars() && !getenv("HQ_NOFOLD") &&
+                      (size_t)h->sgrid * (N + 1) * NV2 <= (size_t)48 * (32u << h->nW);
+    double *blkp[2] = {h->d_blk, h->d_blk + V2S_TOTAL};
+    double *part[2] = {h->d_partial, h->d_partial + (size_t)std::max(h->grid, h->sgrid) * HQ_NL * HQ_NV};
+    int cur = 0, pw = 0, pc_prev = 0;
+    uint32_t pa_prev = 0;
+    bool pending = false;
+    auto resolve = [&]() -> cudaError_t {   // complete the pending scalar step into blkp[0]
+        if (!pending) return cudaSuccess;
+        pending = false;
+        const int from = cur;
+        cur = 0;
+        o.launches++;
+        return hq2_launch::scalars(N, h->full_lists ? 1 : 0, h->Lam, 1, pc_prev, pa_prev, h->sgrid, part[pw ^ 1],
+                                   blkp[from], s, 1, blkp[0]);
+    };
+
     // convergence checks: the two half-sweeps before a check record |dp|
     int next_check = N + 2 * 12;
     double prev_proxy = -1.0;
@@ -1207,12 +1247,27 @@ static hq_status solve_v2(hq_problem *h, double tol, int max_iter, double *pi, c
         sa.P = h->d_pw + (c ? half : 0);
         sa.Q = h->d_pw + (c ? 0 : half);
         sa.omkap = h->d_omkap + (c ? half : 0);
-        sa.partial = h->d_partial;
+        sa.partial = fold ? part[pw] : h->d_partial;
+        sa.coef = fold ? blkp[cur] : h->d_blk;
+        FoldArgs fa;
+        if (fold && pending) {
+            fa.fold = 1;
+            fa.prev_c = pc_prev;
+            fa.prev_active = pa_prev;
+            fa.prev_partial = part[pw ^ 1];
+            fa.blk_out = blkp[cur ^ 1];
+        }
         const bool checking = tol > 0.0 && t >= next_check - 1;
         HQ_CUDA(cudaEventRecord(h->event(2 * (size_t)o.halfsweeps), s));
-        HQ_CUDA(tiled_sweep(h, sa, checking ? 1 : 0, s));
+        HQ_CUDA(tiled_sweep(h, sa, checking ? 1 : 0, s, &fa));
         HQ_CUDA(cudaEventRecord(h->event(2 * (size_t)o.halfsweeps + 1), s));
-        if (h->path != 3 || !hq3_launch::fused_scalars()) {   // path 3: scalar step in the sweep's last CTA
+        if (fold) {
+            if (pending) cur ^= 1;
+            pending = true;
+            pc_prev = c;
+            pa_prev = active;
+            pw ^= 1;
+        } else if (h->path != 3 || !hq3_launch::fused_scalars()) {   // path 3 fused: scalar step in the sweep's last CTA
             HQ_CUDA(hq2_launch::scalars(N, sa.full_lists, h->Lam, 1, c, active, h->sgrid, h->d_partial, h->d_blk, s,
                                         h->path == 3 ? 1 : 0));
             o.launches++;
@@ -1223,6 +1278,7 @@ static hq_status solve_v2(hq_problem *h, double tol, int max_iter, double *pi, c
             if ((active >> n) & 1u) o.updates += binom(N, n);
         if ((active >> (N - 1)) & 1u) o.sweeps = (t - (N - 1)) / 2 + 1;
         if (!checking || t < next_check) continue;
+        HQ_CUDA(resolve());
         HQ_CUDA(cudaMemcpyAsync(h->h_blk, h->d_blk, sizeof(double) * V2S_TOTAL, cudaMemcpyDeviceToHost, s));
         HQ_CUDA(cudaStreamSynchronize(s));
         if (h->h_blk[V2S_MISC + 0] != 0.0) {
@@ -1240,6 +1296,7 @@ static hq_status solve_v2(hq_problem *h, double tol, int max_iter, double *pi, c
         prev_check = t;
         double level = proxy;
         if (proxy <= 2.0 * tol) {
+            sa.coef = h->d_blk;
             st = v2_residual(h, s, sa, o);
             if (st != HQ_OK) return st;
             if (o.res <= tol) {
@@ -1256,6 +1313,8 @@ static hq_status solve_v2(hq_problem *h, double tol, int max_iter, double *pi, c
         }
         next_check = t + gap;
     }
+    HQ_CUDA(resolve());
+    sa.coef = h->d_blk;
     if (!o.converged) {
         st = v2_residual(h, s, sa, o);
         if (st != HQ_OK) return st;

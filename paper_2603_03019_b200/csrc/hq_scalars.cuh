@@ -15,6 +15,37 @@
 #include "hq_internal.h"
 #include "hq_v2.h"
 
+// Per-layer sums of the transposed CTA partials partial[(L * HQ_NV + v) * G + cta] of a
+// sweep launch, layers 0..N: a group of tpi = 2^lg threads per (layer, value) (lg 0..5),
+// each thread with four interleaved accumulators (loads in flight), combined in a fixed
+// order (deterministic).  No barrier.
+__device__ __forceinline__ void reduce_partials_t(const double *partial, int G, int N, double (*S)[NV2], int lg) {
+    const int items = (N + 1) * NV2;
+    const int tpi = 1 << lg, q = threadIdx.x & (tpi - 1);
+    // items rounded up to whole warps: every warp visits its items together, so the
+    // shuffles below are warp-uniform (blockDim.x is a multiple of 32)
+    const int per_warp = 32 >> lg;
+    const int nit = (items + per_warp - 1) / per_warp * per_warp;
+    for (int it = threadIdx.x >> lg; it < nit; it += blockDim.x >> lg) {
+        const int L = it / NV2, v = it - L * NV2;
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        if (L <= N) {
+            const double *src = partial + ((size_t)L * HQ_NV + v) * G;
+            int b = q;
+            for (; b + 3 * tpi < G; b += 4 * tpi) {
+                s0 += src[b];
+                s1 += src[b + tpi];
+                s2 += src[b + 2 * tpi];
+                s3 += src[b + 3 * tpi];
+            }
+            for (; b < G; b += tpi) s0 += src[b];
+        }
+        double s = (s0 + s1) + (s2 + s3);
+        for (int o = 1; o < tpi; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (q == 0 && L <= N) S[L][v] = s;
+    }
+}
+
 __device__ __forceinline__ void scalars_update(int N, int full_lists, double Lam, int mode, int c, uint32_t active,
                                                const double (*S)[NV2], double *sb) {
     double *lam = sb + V2S_LAM, *mu = sb + V2S_MU, *al = sb + V2S_ALPHA, *be = sb + V2S_BETA;

@@ -663,18 +663,13 @@ __global__ void __launch_bounds__(WARPS * 32, 2) k_sweep2(S2Args a) {
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(1024) k_scalars2(int N, int full_lists, double Lam, int mode, int c, uint32_t active,
                                                     int ncta, const double *__restrict__ partial,
-                                                    double *__restrict__ blk, int transposed) {
+                                                    const double *blk, double *blk_out, int transposed) {
     __shared__ double S[HQ_NL][NV2];
+    __shared__ double sblk[V2S_TOTAL];
     const int lane = threadIdx.x & 31, n = threadIdx.x >> 5;
-    if (transposed) {   // partial[(layer * HQ_NV + v) * ncta + cta]: one warp per (layer, value), coalesced
-        for (int i = n; i < HQ_NL * NV2; i += (int)(blockDim.x >> 5)) {
-            const int L = i / NV2, v = i - L * NV2;
-            const double *src = partial + ((size_t)L * HQ_NV + v) * ncta;
-            double s = 0.0;
-            for (int b = lane; b < ncta; b += 32) s += src[b];
-            s = warp_sum(s);
-            if (lane == 0) S[L][v] = s;
-        }
+    for (int i = threadIdx.x; i < V2S_TOTAL; i += blockDim.x) sblk[i] = blk[i];
+    if (transposed) {   // partial[(layer * HQ_NV + v) * ncta + cta]
+        reduce_partials_t(partial, ncta, N, S, 5);   // one warp per (layer, value)
     } else if (n <= N) {
         double s[NV2];
 #pragma unroll
@@ -689,12 +684,9 @@ __global__ void __launch_bounds__(1024) k_scalars2(int N, int full_lists, double
         }
     }
     __syncthreads();
-    // the scalar step runs on a shared-memory copy of the block (one thread, serial)
-    __shared__ double sblk[V2S_TOTAL];
-    for (int i = threadIdx.x; i < V2S_TOTAL; i += blockDim.x) sblk[i] = blk[i];
-    __syncthreads();
+    // the scalar step runs on a shared-memory copy of the block
     scalars_update(N, full_lists, Lam, mode, c, active, S, sblk);
-    for (int i = threadIdx.x; i < V2S_TOTAL; i += blockDim.x) blk[i] = sblk[i];
+    for (int i = threadIdx.x; i < V2S_TOTAL; i += blockDim.x) blk_out[i] = sblk[i];
 }
 
 // pi[m_abi] = p(w(m)) p_{w(m)}(m), internal index m -> ABI index via perm.
@@ -768,8 +760,9 @@ cudaError_t prog_max(const uint32_t *size16, uint32_t *out, uint64_t n, void *tm
     return cub::DeviceReduce::Max(tmp, *tmp_bytes, size16, out, (int)n, s);
 }
 cudaError_t scalars(int N, int full_lists, double Lam, int mode, int c, uint32_t active, int ncta,
-                    const double *partial, double *blk, cudaStream_t s, int transposed) {
-    hq2::k_scalars2<<<1, 1024, 0, s>>>(N, full_lists, Lam, mode, c, active, ncta, partial, blk, transposed);
+                    const double *partial, double *blk, cudaStream_t s, int transposed, double *blk_out) {
+    hq2::k_scalars2<<<1, 1024, 0, s>>>(N, full_lists, Lam, mode, c, active, ncta, partial, blk,
+                                       blk_out ? blk_out : blk, transposed);
     return cudaGetLastError();
 }
 cudaError_t assemble(int N, const double *pw, const double *pn1, const int *perm, double *pi, int grid,

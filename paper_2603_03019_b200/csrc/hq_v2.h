@@ -91,7 +91,8 @@ cudaError_t sweep(const S2Args &a, int mode, int grid, cudaStream_t s);
 cudaError_t prog_max(const uint32_t *size16, uint32_t *out, uint64_t n, void *tmp, size_t *tmp_bytes, cudaStream_t s);
 size_t sweep_smem(uint32_t maxrec);
 cudaError_t scalars(int N, int full_lists, double Lam, int mode, int c, uint32_t active, int ncta,
-                    const double *partial, double *blk, cudaStream_t s, int transposed = 0);
+                    const double *partial, double *blk, cudaStream_t s, int transposed = 0,
+                    double *blk_out = nullptr);   // blk_out: write the updated block there instead of in place
 cudaError_t assemble(int N, const double *pw, const double *pn1, const int *perm, double *pi, int grid,
                      cudaStream_t s);
 int sweep_grid(int nsm);

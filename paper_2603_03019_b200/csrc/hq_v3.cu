@@ -243,7 +243,9 @@ __device__ __forceinline__ double2 ldg_ef(const double2 *p) {
 
 
 
-template <int MODE, bool FULL, bool WP>
+// ST: every program block is staged (host-checked S3Args::all_staged): program reads are
+// plain shared-memory loads with 32-bit addressing
+template <int MODE, bool FULL, bool WP, bool ST>
 __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
     using SL = Slots<MODE, FULL>;
     constexpr int NB = SL::NB;
@@ -265,41 +267,6 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
     const int nthr = 32 << nW;
     double *fscr = sb + (size_t)3 * NB * nthr + (size_t)warp * 32 * 3;
 
-    if (tid < 32) {
-        if (MODE == 2) {
-            const double *pn1 = a.coef + V2S_PN;   // pn1[n + 1] = p(n)
-            s_x[tid] = pn1[tid];
-            s_y[tid] = tid + 2 < 34 ? pn1[tid + 2] : 0.0;
-            s_z[tid] = pn1[tid + 1];
-        } else {
-            s_x[tid] = a.coef[V2S_ALPHA + tid];
-            s_y[tid] = a.coef[V2S_BETA + tid];
-            s_z[tid] = 0.0;
-        }
-        if (tid < R)
-            s_mr[tid] = ((tid & 1) ? a.nu[1] : 0.0) + ((tid & 2) ? a.nu[7] : 0.0) + ((tid & 4) ? a.nu[8] : 0.0);
-    }
-    for (int i = tid; i < 32 * 32; i += blockDim.x) {   // pext of lane bits: s_pext[M * 32 + l]
-        const uint32_t M = (uint32_t)i >> 5, l = (uint32_t)i & 31u;
-        uint32_t r = 0;
-        for (int b = 0, j = 0; b < 5; b++)
-            if ((M >> b) & 1u) r |= ((l >> b) & 1u) << j++;
-        s_pext[i] = (uint8_t)r;
-    }
-    for (int i = tid; i < 16 * 16; i += blockDim.x) {
-        const uint32_t M = (uint32_t)i >> 4, w = (uint32_t)i & 15u;
-        uint32_t r = 0;
-        for (int b = 0, j = 0; b < 4; b++)
-            if ((M >> b) & 1u) r |= ((w >> b) & 1u) << j++;
-        s_pextw[i] = (uint8_t)r;
-    }
-    if (tid == 0) {
-        mbar_init(sptr(&tbar[0]), 1);
-        mbar_init(sptr(&tbar[1]), 1);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    __syncthreads();
-
     // tiles of this CTA: a contiguous range of the popcount-sorted visit order, cut by the
     // host so that every CTA gets the same estimated work
     const uint32_t i0 = __ldg(a.range + blockIdx.x), i1 = __ldg(a.range + blockIdx.x + 1);
@@ -320,8 +287,55 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
         bulk_g2s(sptr(b), a.Q + ((size_t)t << T), TS * 8u, bar);
         if (staged) bulk_g2s(sptr(b + TS), a.prog + o, nrec * 16u, bar);
     };
+    if (tid == 0) {
+        mbar_init(sptr(&tbar[0]), 1);
+        mbar_init(sptr(&tbar[1]), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        if (nt > 0) load_tile(0);   // in flight during the prologue
+    }
 
-    if (tid == 0 && nt > 0) load_tile(0);
+    const double *coef = a.coef;
+    if (MODE < 2 && a.fold) {   // scalar step of the previous half-sweep, redundantly per CTA
+        // in the second tile buffer: consumed before load_tile(1) overwrites it
+        double(*s_S)[NV2] = reinterpret_cast<double(*)[NV2]>(tileq + BUFD);
+        double *s_blk = tileq + BUFD + HQ_NL * NV2;
+        for (int i = tid; i < V2S_TOTAL; i += blockDim.x) s_blk[i] = a.coef[i];
+        reduce_partials_t(a.prev_partial, gridDim.x, a.N, s_S, 2);
+        __syncthreads();
+        scalars_update(a.N, a.full_lists, a.Lam, 1, a.prev_c, a.prev_active, s_S, s_blk);
+        if (blockIdx.x == 0)
+            for (int i = tid; i < V2S_TOTAL; i += blockDim.x) a.blk_out[i] = s_blk[i];
+        coef = s_blk;
+    }
+    if (tid < 32) {
+        if (MODE == 2) {
+            const double *pn1 = a.coef + V2S_PN;   // pn1[n + 1] = p(n)
+            s_x[tid] = pn1[tid];
+            s_y[tid] = tid + 2 < 34 ? pn1[tid + 2] : 0.0;
+            s_z[tid] = pn1[tid + 1];
+        } else {
+            s_x[tid] = coef[V2S_ALPHA + tid];
+            s_y[tid] = coef[V2S_BETA + tid];
+            s_z[tid] = 0.0;
+        }
+        if (tid < R)
+            s_mr[tid] = ((tid & 1) ? a.nu[1] : 0.0) + ((tid & 2) ? a.nu[7] : 0.0) + ((tid & 4) ? a.nu[8] : 0.0);
+    }
+    for (int i = tid; i < 32 * 32; i += blockDim.x) {   // pext of lane bits: s_pext[M * 32 + l]
+        const uint32_t M = (uint32_t)i >> 5, l = (uint32_t)i & 31u;
+        uint32_t r = 0;
+        for (int b = 0, j = 0; b < 5; b++)
+            if ((M >> b) & 1u) r |= ((l >> b) & 1u) << j++;
+        s_pext[i] = (uint8_t)r;
+    }
+    for (int i = tid; i < 16 * 16; i += blockDim.x) {
+        const uint32_t M = (uint32_t)i >> 4, w = (uint32_t)i & 15u;
+        uint32_t r = 0;
+        for (int b = 0, j = 0; b < 4; b++)
+            if ((M >> b) & 1u) r |= ((w >> b) & 1u) << j++;
+        s_pextw[i] = (uint8_t)r;
+    }
+    __syncthreads();   // barriers initialised (thread 0) before any wait
 
     // ---- per-thread constants
     double mu_t = 0.0;   // busy lane and warp units of this thread (tile units: mu_F of the program)
@@ -382,6 +396,20 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
         const uint32_t t = __ldg(a.order + tidx);
         const uint32_t jt = t << T;
         const int buf = k & 1;
+#ifdef HQ_HLOOP3
+        // tile-unit neighbour slices: three rotating buffers, each refilled right after it is
+        // consumed (two units of loads in flight ahead of the one accumulated, no copies)
+        const double *qb = a.Q + (jt | jw);
+        auto hload = [&](int h, double2 (&B)[4]) {
+            const size_t off = (size_t)1 << (T + h);
+            const double *src = ((t >> h) & 1u) ? qb - off : qb + off;
+#pragma unroll
+            for (int kk = 0; kk < 4; kk++) B[kk] = ldg2(src + (kk << 6), pol_el);
+        };
+        double2 B0[4], B1[4], B2[4];
+        if (nH > 0) hload(0, B0);
+        if (nH > 1) hload(1, B1);
+#else
         // tile-unit neighbour slices: two units of loads in flight ahead of the one accumulated
         auto hsrc = [&](int h) -> const double * { return a.Q + ((jt ^ (1u << (T + h))) | jw); };
         double2 pa[4], pb2[4];
@@ -393,6 +421,7 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
 #pragma unroll
             for (int kk = 0; kk < 4; kk++) pb2[kk] = ldg2(hsrc(1) + (kk << 6), pol_el);
         }
+#endif
         mbar_wait(sptr(&tbar[buf]), (unsigned)((k >> 1) & 1));
         __syncthreads();   // every warp is done with tile k-1: its buffer may be refilled
         if (tid == 0 && k + 1 < nt) {
@@ -408,7 +437,7 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
             const uint64_t widx = (uint64_t)tidx << nW;
             const uint32_t o0 = __ldg(a.off16 + widx), ow = __ldg(a.off16 + widx + warp);
             const uint32_t nrec = (widx + nwarps < nwt ? __ldg(a.off16 + widx + nwarps) : a.total16) - o0;
-            P.pg = nrec <= a.maxblk16 ? reinterpret_cast<const uint4 *>(tq + TS) + (ow - o0) : a.prog + ow;
+            P.pg = (ST || nrec <= a.maxblk16) ? reinterpret_cast<const uint4 *>(tq + TS) + (ow - o0) : a.prog + ow;
             P.pl = s_pext + lane;
             P.pw = s_pextw + warp;
         }
@@ -462,6 +491,9 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
                 else D[r] = fma(nuu, q[r], D[r]);
             }
         }
+#ifdef HQ_HLOOP3
+        if (nH > 2) hload(2, B2);   // qo is dead: room for the third buffer
+#endif
         // ---- lane units 2..6 (lane bits 0..4): busy per lane
 #pragma unroll
         for (int b = 0; b < 5; b++) {
@@ -504,6 +536,40 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
                 for (int r = 0; r < R; r++) D[r] = fma(nuu, q[r], D[r]);
             }
         }
+#ifdef HQ_HLOOP3
+        // ---- tile units (H): neighbour tile slices straight from global memory (L2)
+        auto unit_H = [&](int h, const double2 (&B)[4]) {
+            const int u = NVU + h;
+            double qh[R];
+#pragma unroll
+            for (int kk = 0; kk < 4; kk++) {
+                qh[2 * kk] = B[kk].x;
+                qh[2 * kk + 1] = B[kk].y;
+            }
+            if ((t >> h) & 1u) {
+                const uint4 hu = P.hdr(u);
+                const double Wt = unit_rates(P, hu, sh, hdr_w0(hu), qh, A);
+#pragma unroll
+                for (int r = 0; r < R; r++) A[r] = fma(Wt, qh[r], A[r]);
+            } else {
+                const double nuu = a.nu[u];
+#pragma unroll
+                for (int r = 0; r < R; r++) D[r] = fma(nuu, qh[r], D[r]);
+            }
+        };
+        for (int h = 0; h < nH; h += 3) {
+            unit_H(h, B0);
+            if (h + 3 < nH) hload(h + 3, B0);
+            if (h + 1 < nH) {
+                unit_H(h + 1, B1);
+                if (h + 4 < nH) hload(h + 4, B1);
+            }
+            if (h + 2 < nH) {
+                unit_H(h + 2, B2);
+                if (h + 5 < nH) hload(h + 5, B2);
+            }
+        }
+#else
         // ---- tile units (H): neighbour tile slices straight from global memory (L2), two
         //      units of loads in flight; unrolled by two so the buffers alternate in place
         auto unit_H = [&](int h, double2 (&buf)[4]) {
@@ -533,6 +599,7 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
             unit_H(h, pa);
             if (h + 1 < nH) unit_H(h + 1, pb2);
         }
+#endif
         // ---- lambda_m: Lambda minus the atoms whose whole (truncated) list is busy
         double lam[R];
         if (FULL) {
@@ -990,29 +1057,35 @@ cudaError_t prog_write(const P3Args &a, const uint32_t *order, const uint32_t *o
     return cudaGetLastError();
 }
 
-template <int MODE, bool FULL, bool WP>
+template <int MODE, bool FULL, bool WP, bool ST>
 static cudaError_t launch(const S3Args &a, int grid, cudaStream_t s) {
     const size_t sm = sweep_smem(a.nW, a.maxblk16, a.nslots);
-    cudaError_t e = cudaFuncSetAttribute(hq3::k_sweep3<MODE, FULL, WP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    auto kern = hq3::k_sweep3<MODE, FULL, WP, ST>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
     // leave the rest of the unified L1/shared array to L1
     const int carve = (int)std::min<size_t>(100, (sm + 2048) * 100 / (228 * 1024) + 1);
-    e = cudaFuncSetAttribute(hq3::k_sweep3<MODE, FULL, WP>, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
     if (e != cudaSuccess) return e;
-    hq3::k_sweep3<MODE, FULL, WP><<<grid, 32 << a.nW, sm, s>>>(a);
+    kern<<<grid, 32 << a.nW, sm, s>>>(a);
     return cudaGetLastError();
+}
+
+template <bool WP, bool ST>
+static cudaError_t sweep_st(const S3Args &a, int full, int mode, int grid, cudaStream_t s) {
+    if (full) {
+        if (mode == 0) return launch<0, true, WP, ST>(a, grid, s);
+        if (mode == 1) return launch<1, true, WP, ST>(a, grid, s);
+        return launch<2, true, WP, false>(a, grid, s);
+    }
+    if (mode == 0) return launch<0, false, WP, ST>(a, grid, s);
+    if (mode == 1) return launch<1, false, WP, ST>(a, grid, s);
+    return launch<2, false, WP, false>(a, grid, s);
 }
 
 template <bool WP>
 static cudaError_t sweep_wp(const S3Args &a, int full, int mode, int grid, cudaStream_t s) {
-    if (full) {
-        if (mode == 0) return launch<0, true, WP>(a, grid, s);
-        if (mode == 1) return launch<1, true, WP>(a, grid, s);
-        return launch<2, true, WP>(a, grid, s);
-    }
-    if (mode == 0) return launch<0, false, WP>(a, grid, s);
-    if (mode == 1) return launch<1, false, WP>(a, grid, s);
-    return launch<2, false, WP>(a, grid, s);
+    return a.all_staged ? sweep_st<WP, true>(a, full, mode, grid, s) : sweep_st<WP, false>(a, full, mode, grid, s);
 }
 
 cudaError_t sweep(const S3Args &a, int full, int mode, int grid, cudaStream_t s) {

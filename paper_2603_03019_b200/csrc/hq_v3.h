@@ -60,7 +60,16 @@ struct S3Args {
     unsigned *done;          // CTA completion counter (self-resetting)
     int full_lists;
     int warp_programs;       // 1: one rate program per warp tile (tables over lane bits only)
+    int all_staged;          // 1: every tile's program block fits the staged capacity (maxblk16)
     unsigned long long *wtime;   // -DHQ_WARP_TIMING builds: busy cycles per (CTA, warp)
+    // folded scalar step (MODE 0/1): every CTA first performs the scalar step of the previous
+    // half-sweep (class prev_c, layers prev_active) from that launch's transposed partials
+    // prev_partial and the block coef; CTA 0 stores the updated block in blk_out
+    int fold;
+    int prev_c;
+    uint32_t prev_active;
+    const double *prev_partial;
+    double *blk_out;
 };
 
 struct P3Args {   // program precompute (one program per warp tile or per CTA tile)

@@ -44,10 +44,15 @@ print(json.dumps(out))
 res = {n: [] for n in names}
 for rnd in range(2):   # two interleaved rounds of fresh processes
     for n in names:
-        lib, _, prog = n.partition("@")   # NAME@cta / NAME@warp forces the program granularity
+        # NAME@cta / NAME@warp forces the program granularity; NAME@VAR=VALUE sets an env var
+        lib, *mods = n.split("@")
         env = dict(os.environ, ROOT=ROOT, CFG=str(cfg), REPS=str(reps), HQ_LIB=os.path.join(VAR, f"libhq_{lib}.so"))
-        if prog:
-            env["HQ_PROG"] = prog
+        for mod in mods:
+            k, eq, v = mod.partition("=")
+            if eq:
+                env[k] = v
+            else:
+                env["HQ_PROG"] = mod
         p = subprocess.run([sys.executable, "-c", child], env=env, capture_output=True, text=True, timeout=600)
         if p.returncode != 0:
             print(n, "FAILED", p.stderr[-2000:])
