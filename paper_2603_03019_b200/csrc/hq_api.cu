@@ -450,6 +450,8 @@ extern "C" hq_status hq_create(int N, int J, const double *lambda, const double 
         h->path = N < 8 ? 1 : (N < 9 || (penv && std::string(penv) == "2")) ? 2 : 3;
         if (h->path == 3) {
             h->nW = hq3_launch::choose_nw(N);
+            if (const char *wenv = getenv("HQ_NW"))   // development override (log2 warps per CTA)
+                h->nW = std::max(0, std::min({atoi(wenv), 4, N - 9}));
             h->perm = choose_perm_v3(N, abi, h->nW);
         } else {
             h->perm = choose_perm(N, abi);
@@ -486,7 +488,7 @@ static hq_status ensure_device(hq_problem *h) {
     auto alloc = [&](void **p, size_t bytes) -> cudaError_t { return cudaMalloc(p, bytes ? bytes : 16); };
     if (h->path == 3) {
         const uint64_t nt3 = 1ull << (N - 9 - h->nW);
-        h->sgrid = (int)std::min<uint64_t>(nt3, (uint64_t)h->nsm * std::max(1, 16 >> h->nW));
+        h->sgrid = (int)std::min<uint64_t>(nt3, (uint64_t)h->nsm * hq3_launch::ctas_per_sm(h->nW));
     } else {
         h->sgrid = hq2_launch::sweep_grid(h->nsm);
     }

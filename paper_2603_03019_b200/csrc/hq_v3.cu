@@ -35,6 +35,7 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <algorithm>
 #include "hq_internal.h"
 #include "hq_v2.h"
@@ -1037,7 +1038,11 @@ size_t sweep_smem(int nW, uint32_t maxblk16, int nslots) {
     return 2 * (TS * 8 + (size_t)maxblk16 * 16) + W * 32 * 3 * 5 * 8 + W * 32 * 3 * 8;
 }
 
-// staged program capacity (records per tile block): as large as fits, at most the largest block
+// CTAs resident per SM the grid is sized for (hq_create: sgrid = nsm * ctas_per_sm)
+int ctas_per_sm(int nW) { return std::max(1, 16 >> nW); }
+
+// staged program capacity (records per tile block): as large as fits, at most the largest
+// block (measured: staging every program beats more resident CTAs per SM)
 uint32_t choose_cap(int nW, uint32_t maxblk16) {
     const size_t budget = 224u * 1024u - 2048u;
     const size_t fixed = sweep_smem(nW, 0, 0);

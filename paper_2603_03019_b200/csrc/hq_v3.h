@@ -94,5 +94,6 @@ size_t sweep_smem(int nW, uint32_t maxblk16, int nslots);
 int choose_slots(int nW, uint32_t maxblk16);
 uint32_t choose_cap(int nW, uint32_t maxblk16);
 int choose_nw(int N);
+int ctas_per_sm(int nW);   // CTAs per SM the sweep grid is sized for
 bool fused_scalars();
 }  // namespace hq3_launch
