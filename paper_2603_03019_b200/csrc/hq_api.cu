@@ -862,6 +862,8 @@ static hq_status v3_programs(hq_problem *h, cudaStream_t s, int nwv, const std::
     std::vector<uint32_t> off16(ntiles << nW);
     std::vector<double> cost(ntiles);
     double tot = 0.0;
+    const int cost_model = getenv("HQ_COST") ? atoi(getenv("HQ_COST")) : 0;   // development switch
+    const double cost_base = getenv("HQ_COST_BASE") ? atof(getenv("HQ_COST_BASE")) : 263.0;
     ps.maxblk = 0;
     for (uint64_t i = 0; i < ntiles; i++) {
         uint32_t b = 0, bmax = 0;
@@ -878,7 +880,8 @@ static hq_status v3_programs(hq_problem *h, cudaStream_t s, int nwv, const std::
         // the evaluation of the program records (every warp evaluates a CTA program).  Chosen
         // by same-box A/B timing; models fitted to per-warp busy cycles balanced worse.
         cost[i] = 256.0 + (double)b * (per_warp ? 1.0 : (double)W / 4.0);
-        (void)bmax;
+        if (cost_model == 1) cost[i] = cost_base + (double)bmax;   // slowest warp's program
+        if (cost_model == 2) cost[i] = cost_base + 0.5 * (double)bmax + 0.5 * (double)b / W;
         tot += cost[i];
     }
     HQ_CUDA(cudaMemcpyAsync(ps.off16, off16.data(), 4 * off16.size(), cudaMemcpyHostToDevice, s));

@@ -287,6 +287,10 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
         mbar_expect(bar, TS * 8u + (staged ? nrec * 16u : 0u));
         bulk_g2s(sptr(b), a.Q + ((size_t)t << T), TS * 8u, bar);
         if (staged) bulk_g2s(sptr(b + TS), a.prog + o, nrec * 16u, bar);
+#ifndef HQ_NO_OMKAP_PREFETCH
+        // the tile's scatter weights (read once, in the epilogue) into L2 a tile ahead
+        if (MODE < 2) prefetch_l2(a.omkap + ((size_t)t << T), TS * 16u);
+#endif
     };
     if (tid == 0) {
         mbar_init(sptr(&tbar[0]), 1);
