@@ -70,6 +70,17 @@ __device__ __forceinline__ void bulk_g2s(unsigned dst, const void *src, unsigned
                  "l"(src), "r"(bytes), "r"(bar)
                  : "memory");
 }
+// bulk copy with an L2 cache policy (read-once data: evict-first)
+__device__ __forceinline__ void bulk_g2s_pol(unsigned dst, const void *src, unsigned bytes, unsigned bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(bar), "l"(pol)
+        : "memory");
+}
+// 16-byte store with an L2 cache policy
+__device__ __forceinline__ void stg2_pol(double *p, double x, double y, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(x), "d"(y), "l"(pol) : "memory");
+}
 #ifdef HQ_DEBUG_HANG
 // bounded wait: reports the barrier and traps instead of hanging (debug builds)
 __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
@@ -285,9 +296,17 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
         const unsigned bar = sptr(&tbar[buf]);
         double *b = tileq + (size_t)buf * BUFD;
         mbar_expect(bar, TS * 8u + (staged ? nrec * 16u : 0u));
+#ifndef HQ_NO_L2POL
+        bulk_g2s_pol(sptr(b), a.Q + ((size_t)t << T), TS * 8u, bar, pol_evict_last());
+#else
         bulk_g2s(sptr(b), a.Q + ((size_t)t << T), TS * 8u, bar);
+#endif
+#ifndef HQ_NO_L2POL
+        if (staged) bulk_g2s_pol(sptr(b + TS), a.prog + o, nrec * 16u, bar, pol_evict_first());
+#else
         if (staged) bulk_g2s(sptr(b + TS), a.prog + o, nrec * 16u, bar);
-#ifndef HQ_NO_OMKAP_PREFETCH
+#endif
+#ifdef HQ_OMKAP_PREFETCH
         // the tile's scatter weights (read once, in the epilogue) into L2 a tile ahead
         if (MODE < 2) prefetch_l2(a.omkap + ((size_t)t << T), TS * 16u);
 #endif
@@ -689,7 +708,11 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
             for (int kk = 0; kk < 4; kk++) {
                 double *dst = a.P + (jt + (jw | (kk << 6)));
                 if (act[2 * kk] && act[2 * kk + 1]) {
+#ifndef HQ_NO_L2POL
+                    stg2_pol(dst, pnew[2 * kk], pnew[2 * kk + 1], pol_ef);
+#else
                     *reinterpret_cast<double2 *>(dst) = make_double2(pnew[2 * kk], pnew[2 * kk + 1]);
+#endif
                 } else {
                     if (act[2 * kk]) dst[0] = pnew[2 * kk];
                     if (act[2 * kk + 1]) dst[1] = pnew[2 * kk + 1];
