@@ -881,6 +881,7 @@ static hq_status v3_programs(hq_problem *h, cudaStream_t s, int nwv, const std::
         // by same-box A/B timing; models fitted to per-warp busy cycles balanced worse.
         cost[i] = 256.0 + (double)b * (per_warp ? 1.0 : (double)W / 4.0);
         if (cost_model == 1) cost[i] = cost_base + (double)bmax;   // slowest warp's program
+        if (cost_model == 3) cost[i] = cost_base + (double)b;      // per-tile base in records
         if (cost_model == 2) cost[i] = cost_base + 0.5 * (double)bmax + 0.5 * (double)b / W;
         tot += cost[i];
     }

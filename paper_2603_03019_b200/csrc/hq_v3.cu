@@ -318,6 +318,10 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
         if (nt > 0) load_tile(0);   // in flight during the prologue
     }
 
+#ifdef HQ_WARP_TIMING
+    unsigned long long t_start;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+#endif
     const double *coef = a.coef;
     if (MODE < 2 && a.fold) {   // scalar step of the previous half-sweep, redundantly per CTA
         // in the second tile buffer: consumed before load_tile(1) overwrites it
@@ -721,6 +725,14 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
         }
     }
     flush();
+#ifdef HQ_WARP_TIMING
+    if (MODE == 0 && tid == 0) {   // CTA start / end (globaltimer ns), after the per-warp slots
+        unsigned long long t_end;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+        a.wtime[2368 + 2 * blockIdx.x] = t_start;
+        a.wtime[2368 + 2 * blockIdx.x + 1] = t_end;
+    }
+#endif
     // ---- CTA partials: warp w's lane L holds layer L; fixed-order sum over warps
     __syncthreads();   // every copy consumed: reuse the tile buffers
     double *red = tileq;

@@ -45,3 +45,11 @@ coef, *_ = np.linalg.lstsq(Xm, meas, rcond=None)
 print("fit: cycles = %.0f per tile + %.1f per max-warp record  -> base = %.0f records" % (coef[0], coef[1], coef[0] / coef[1]))
 fit = Xm @ coef
 print("fit corr:", round(np.corrcoef(fit, meas)[0, 1], 3))
+
+# CTA start / end times of the last MODE-0 launch (globaltimer, ns)
+se = hq.hq_debug_copy(s.h, 7, 8 * 4096, np.uint64)[2368:2368 + 2 * G].reshape(G, 2).astype(np.int64)
+t0 = se[:, 0].min()
+dur = se[:, 1] - se[:, 0]
+print("CTA start spread us:", (se[:, 0].max() - t0) / 1e3, " durations us mean/max:", dur.mean() / 1e3, dur.max() / 1e3,
+      " last end us:", (se[:, 1].max() - t0) / 1e3)
+print("CTA end times (us, sorted, every 10th):", np.round(np.sort(se[:, 1] - t0)[::10] / 1e3, 1))
