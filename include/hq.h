@@ -116,6 +116,48 @@ hq_status hq_solve(hq_handle h, double tol, int max_iter, double *pi, void *cuda
 hq_status hq_measures(hq_handle h, const double *pi, double *workload, double *dispatch, double *loss,
                       void *cuda_stream);
 
+/*
+ * hq_set_buffer -- give calls that find every unit busy a waiting room
+ * (SURVEY.md §8(f) row f1).
+ *
+ *   C  0 (default): loss system, the model above.
+ *      C > 0: finite buffer of C waiting calls (Proposition "Reformulation,
+ *      Finite Buffer"): a call arriving when all N units
+ *      are busy waits if fewer than C calls wait, otherwise it is lost;
+ *      waiting calls are served first-come-first-served.
+ *      HQ_BUFFER_UNLIMITED: unlimited waiting room (Remark);
+ *      hq_solve then needs Lambda < sum of the service rates.
+ *
+ * Needs full preference lists (every row of pref ranks all N units): a call
+ * queues exactly when all N units are busy.  The
+ * conditional probabilities p_n(B_m) are those of the loss system (the
+ * proposition's update equations are unchanged); hq_solve then returns the
+ * hypercube part P{B_m} = p(w(B_m)) p_w(B_m)(B_m) with the layer masses p(n)
+ * of the extended birth-death chain, lambda(n) = Lambda and mu(n) = sum nu for
+ * n > N, i.e. the loss-system pi scaled by 1 / (1 + P{all busy} sum_c r^c),
+ * r = Lambda / sum nu.  residual_out stays the residual of the hypercube block,
+ * an upper bound of the residual of the whole chain (the tail states satisfy
+ * their balance equations in closed form; R15).  hq_measures
+ * reports: workload includes the waiting states (all units busy); loss =
+ * P~{C} (0 when unlimited); dispatch counts a queued call for the unit that
+ * completes service first (unit i with probability nu_i / sum nu, DESIGN.md
+ * R14), so sum_ij rho_ij = 1 and nu_i rho_i = Lambda (1 - loss) sum_j rho_ij.
+ *
+ * Takes effect at the next hq_solve (it invalidates the last one).
+ * Errors: HQ_E_INVAL (C < HQ_BUFFER_UNLIMITED, or C != 0 with truncated lists).
+ */
+#define HQ_BUFFER_UNLIMITED (-1)
+hq_status hq_set_buffer(hq_handle h, int C);
+
+/*
+ * hq_queue_tail -- after hq_solve with a waiting room: tail[c-1] = P~{c}, the
+ * probability that c calls wait (P~{c} = p(N + c)), for
+ * c = 1..len (host array, caller-owned; len <= C for a finite buffer; any len
+ * when unlimited).  mass (host, may be NULL) receives sum_{c>=1} P~{c}.  With
+ * C = 0 the tail is zero.  Errors: HQ_E_INVAL, HQ_E_ORDER (no solve yet).
+ */
+hq_status hq_queue_tail(hq_handle h, double *tail, int len, double *mass);
+
 /* Release every device and host resource of h (NULL is a no-op). */
 void hq_destroy(hq_handle h);
 
@@ -135,7 +177,7 @@ const char *hq_error_string(hq_handle h);
  *   rate programs, [13] code path (1: N < 8 two-pass, 2: warp-tiled, 3: CTA-tiled),
  *   [14] largest rate-program block of a CTA tile (16-byte records),
  *   [15] warp bits varying inside a rate program (0: one program per warp tile,
- *        nW: one program per CTA tile; chosen by timing both at the first solve),
+ *        the default; nW: one program per CTA tile, HQ_PROG=cta),
  *   [16], [17] timed sweep launches (ms) with CTA / warp programs at that choice
  *        (0: not timed).
  */

@@ -38,6 +38,10 @@ cudaError_t assemble(int N, const double *pw, const double *pn, double *pi, int 
 cudaError_t zeta(int N, double *g, int grid, cudaStream_t s);
 cudaError_t measures(int N, int J, const double *lam, double Lam, const int32_t *pref, const double *g,
                      double *workload, double *dispatch, double *loss, cudaStream_t s);
+cudaError_t scale(double *x, uint64_t n, double f, int grid, cudaStream_t s);
+cudaError_t buffer_measures(int N, int J, const double *lam, double Lam, const double *nu, const double *pi_all_busy,
+                            const double *loss_dev, double tail_mass, double tail_last, double loss_q,
+                            double *workload, double *dispatch, cudaStream_t s);
 int tile_states();
 cudaError_t init_v2(const KArgs &k, int grid, cudaStream_t s);
 }  // namespace hqk_launch
@@ -289,6 +293,12 @@ struct hq_problem {
     int device = -1;
     int nsm = 0;
     bool solved = false;
+    // waiting room (hq_set_buffer): 0 loss system, C > 0 finite buffer, -1 unlimited
+    int bufC = 0;
+    double q_r = 0.0;        // Lambda / sum nu
+    double q_first = 0.0;    // P~{1} of the last solve
+    double q_mass = 0.0;     // sum_c P~{c}
+    double q_last = 0.0;     // P~{C} (finite C), 0 for an unlimited buffer
     double stats[HQ_STATS_LEN] = {0};
     // device memory
     int2 *d_node = nullptr;
@@ -1333,8 +1343,8 @@ static hq_status solve_v2(hq_problem *h, double tol, int max_iter, double *pi, c
     return HQ_OK;
 }
 
-extern "C" hq_status hq_solve(hq_handle h, double tol, int max_iter, double *pi, void *cuda_stream, int *iters_out,
-                              double *residual_out) {
+static hq_status solve_core(hq_handle h, double tol, int max_iter, double *pi, void *cuda_stream, int *iters_out,
+                            double *residual_out) {
     if (!h) return HQ_E_INVAL;
     if (!pi) {
         h->err = "pi is NULL";
@@ -1545,6 +1555,93 @@ extern "C" hq_status hq_solve(hq_handle h, double tol, int max_iter, double *pi,
     return converged ? HQ_OK : HQ_NOT_CONVERGED;
 }
 
+// Waiting room (Proposition "Reformulation, Finite Buffer", and the
+// Remark on unlimited capacity): the conditional probabilities are those of
+// the loss system, the tail states follow the birth-death chain with lambda(n) = Lambda and
+// mu(n) = sum nu for n > N, so P~{c} = P{all busy} r^c with r = Lambda / sum nu and every
+// hypercube probability is the loss-system one scaled by 1 / (1 + sum_c r^c P{all busy}).
+static hq_status apply_buffer(hq_problem *h, double *pi, cudaStream_t s) {
+    const int N = h->N;
+    const uint64_t S = 1ull << N;
+    double pN = 0.0;
+    HQ_CUDA(cudaMemcpyAsync(&pN, pi + (S - 1), sizeof(double), cudaMemcpyDeviceToHost, s));
+    HQ_CUDA(cudaStreamSynchronize(s));
+    double snu = 0.0;
+    for (int i = 0; i < N; i++) snu += h->mu[i];
+    const double r = h->Lam / snu;
+    double geo = 0.0;   // sum_{c=1}^{C} r^c (C = infinity: r / (1 - r))
+    if (h->bufC < 0) {
+        if (!(r < 1.0)) {
+            h->err = "unlimited buffer needs Lambda < sum of service rates (PAPER.md:296)";
+            return HQ_E_INVAL;
+        }
+        geo = r / (1.0 - r);
+    } else if (h->bufC <= 65536) {
+        double x = 1.0;
+        for (int c = 1; c <= h->bufC; c++) {
+            x *= r;
+            geo += x;
+        }
+    } else {
+        geo = r == 1.0 ? (double)h->bufC : r * std::expm1((double)h->bufC * std::log(r)) / (r - 1.0);
+    }
+    const double sc = 1.0 / (1.0 + pN * geo);
+    HQ_CUDA(hqk_launch::scale(pi, S, sc, h->nsm * 8, s));
+    h->q_r = r;
+    h->q_first = sc * pN * r;
+    h->q_mass = sc * pN * geo;
+    h->q_last = h->bufC < 0 ? 0.0 : sc * pN * std::pow(r, (double)h->bufC);
+    HQ_CUDA(cudaStreamSynchronize(s));
+    return HQ_OK;
+}
+
+extern "C" hq_status hq_solve(hq_handle h, double tol, int max_iter, double *pi, void *cuda_stream, int *iters_out,
+                              double *residual_out) {
+    hq_status st = solve_core(h, tol, max_iter, pi, cuda_stream, iters_out, residual_out);
+    if (h && h->bufC != 0 && (st == HQ_OK || st == HQ_NOT_CONVERGED)) {
+        const hq_status sb = apply_buffer(h, pi, (cudaStream_t)cuda_stream);
+        if (sb != HQ_OK) {
+            h->solved = false;
+            return sb;
+        }
+    }
+    return st;
+}
+
+extern "C" hq_status hq_set_buffer(hq_handle h, int C) {
+    if (!h) return HQ_E_INVAL;
+    if (C < HQ_BUFFER_UNLIMITED) {
+        h->err = "buffer capacity must be >= 0 or HQ_BUFFER_UNLIMITED";
+        return HQ_E_INVAL;
+    }
+    if (C != 0 && !h->full_lists) {
+        h->err = "a waiting room needs full preference lists (a call queues when every unit is busy)";
+        return HQ_E_INVAL;
+    }
+    h->bufC = C;
+    h->solved = false;
+    return HQ_OK;
+}
+
+extern "C" hq_status hq_queue_tail(hq_handle h, double *tail, int len, double *mass) {
+    if (!h || len < 0 || (len > 0 && !tail)) return HQ_E_INVAL;
+    if (!h->solved) {
+        h->err = "hq_queue_tail called before a successful hq_solve";
+        return HQ_E_ORDER;
+    }
+    if (h->bufC > 0 && len > h->bufC) {
+        h->err = "len exceeds the buffer capacity";
+        return HQ_E_INVAL;
+    }
+    double x = h->q_first;
+    for (int c = 0; c < len; c++) {
+        tail[c] = h->bufC == 0 ? 0.0 : x;
+        x *= h->q_r;
+    }
+    if (mass) *mass = h->bufC == 0 ? 0.0 : h->q_mass;
+    return HQ_OK;
+}
+
 extern "C" hq_status hq_measures(hq_handle h, const double *pi, double *workload, double *dispatch, double *loss,
                                  void *cuda_stream) {
     if (!h) return HQ_E_INVAL;
@@ -1566,6 +1663,13 @@ extern "C" hq_status hq_measures(hq_handle h, const double *pi, double *workload
     HQ_CUDA(hqk_launch::zeta(N, g, h->nsm * 8, s));
     HQ_CUDA(hqk_launch::measures(N, h->J, h->d_lam, h->Lam, h->d_pref, g, workload, dispatch,
                                  h->d_small + S_STATS, s));
+    if (h->bufC != 0) {   // waiting room: queued calls (R14), loss = P~{C}
+        HQ_CUDA(hqk_launch::buffer_measures(N, h->J, h->d_lam, h->Lam, h->mu.data(), pi + (S - 1), h->d_small + S_STATS,
+                                            h->q_mass, h->q_last, h->q_last, workload, dispatch, s));
+        HQ_CUDA(cudaStreamSynchronize(s));
+        *loss = h->q_last;
+        return HQ_OK;
+    }
     HQ_CUDA(cudaMemcpyAsync(loss, h->d_small + S_STATS, sizeof(double), cudaMemcpyDeviceToHost, s));
     HQ_CUDA(cudaStreamSynchronize(s));
     return HQ_OK;

@@ -36,6 +36,10 @@ enum {
     FV_SUMP = 2,  // sum p_new
 };
 
+struct NuArg {   // per-unit rates by value (N <= 31)
+    double v[32];
+};
+
 struct DevTrie {
     int nnodes;
     const int2 *node;        // .x = unit of the node, .y = preorder index after its subtree

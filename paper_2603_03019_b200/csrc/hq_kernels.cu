@@ -405,6 +405,38 @@ __global__ void k_measures(int N, int J, const double *__restrict__ lam, double 
     }
 }
 
+// ---- waiting room (finite buffer C > 0 or unlimited), full preference lists
+// (Proposition "Reformulation, Finite Buffer"; Remark).
+// The conditional probabilities p_n(B_m) are those of the loss system; the layer masses
+// follow the extended birth-death chain, so pi of the hypercube states is the loss-system
+// pi scaled by s = 1 / (1 + sum_c G(N + c) / G(N) p(N)).
+__global__ void k_scale(double *__restrict__ x, uint64_t n, double s) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        x[i] *= s;
+}
+
+// Measures of the queued system from those of the hypercube states (k_measures output):
+//   rho_i  += sum_c P~{c}                  (every unit is busy while calls wait)
+//   rho_ij  = [f_j sum_{S_ij} pi + f_j P_wait nu_i / sum nu] / (1 - loss_q)
+// where P_wait = P(all busy, room in the buffer) and a queued call is served by the unit
+// that completes service first (unit i with probability nu_i / sum nu; R14).
+__global__ void k_buffer_measures(int N, int J, const double *__restrict__ lam, double Lam, NuArg nu,
+                                  const double *__restrict__ pi_all_busy, const double *__restrict__ loss_dev,
+                                  double tail_mass, double tail_last, double loss_q, double *__restrict__ workload,
+                                  double *__restrict__ dispatch) {
+    const double pall = *pi_all_busy, ld = *loss_dev;
+    const double pwait = pall + tail_mass - tail_last;
+    double snu = 0.0;
+    for (int i = 0; i < N; i++) snu += nu.v[i];
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < J * N; k += gridDim.x * blockDim.x) {
+        const int j = k / N, i = k - j * N;
+        const double f = lam[j] / Lam;
+        dispatch[k] = (dispatch[k] * (1.0 - ld) + f * pwait * nu.v[i] / snu) / (1.0 - loss_q);
+    }
+    if (blockIdx.x == 0)
+        for (int i = threadIdx.x; i < N; i += blockDim.x) workload[i] += tail_mass;
+}
+
 }  // namespace hqk
 
 // ---------------------------------------------------------------------------
@@ -453,6 +485,19 @@ cudaError_t zeta(int N, double *g, int grid, cudaStream_t s) {
         if (e != cudaSuccess) return e;
     }
     return cudaSuccess;
+}
+cudaError_t scale(double *x, uint64_t n, double f, int grid, cudaStream_t s) {
+    hqk::k_scale<<<grid, 256, 0, s>>>(x, n, f);
+    return cudaGetLastError();
+}
+cudaError_t buffer_measures(int N, int J, const double *lam, double Lam, const double *nu, const double *pi_all_busy,
+                            const double *loss_dev, double tail_mass, double tail_last, double loss_q,
+                            double *workload, double *dispatch, cudaStream_t s) {
+    NuArg a;
+    for (int i = 0; i < 32; i++) a.v[i] = i < N ? nu[i] : 0.0;
+    hqk::k_buffer_measures<<<8, 256, 0, s>>>(N, J, lam, Lam, a, pi_all_busy, loss_dev, tail_mass, tail_last, loss_q,
+                                             workload, dispatch);
+    return cudaGetLastError();
 }
 cudaError_t measures(int N, int J, const double *lam, double Lam, const int32_t *pref, const double *g,
                      double *workload, double *dispatch, double *loss, cudaStream_t s) {

@@ -25,7 +25,8 @@ HQ_STATS_LEN = 20
 STATUS_NAMES = {0: "HQ_OK", 1: "HQ_NOT_CONVERGED", -1: "HQ_E_INVAL", -2: "HQ_E_NOMEM", -3: "HQ_E_CUDA",
                 -4: "HQ_E_NUMERIC", -5: "HQ_E_ORDER"}
 EXPORTED = ["hq_create", "hq_solve", "hq_measures", "hq_destroy", "hq_error_string", "hq_stats", "hq_version",
-            "hq_debug_copy"]
+            "hq_debug_copy", "hq_set_buffer", "hq_queue_tail"]
+HQ_BUFFER_UNLIMITED = -1
 
 _dptr = ctypes.POINTER(ctypes.c_double)
 _lib = None
@@ -65,6 +66,10 @@ def load():
     lib.hq_version.argtypes = []
     lib.hq_debug_copy.restype = ctypes.c_int
     lib.hq_debug_copy.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t]
+    lib.hq_set_buffer.restype = ctypes.c_int
+    lib.hq_set_buffer.argtypes = [ctypes.c_void_p, ctypes.c_int]
+    lib.hq_queue_tail.restype = ctypes.c_int
+    lib.hq_queue_tail.argtypes = [ctypes.c_void_p, _dptr, ctypes.c_int, _dptr]
     _lib = lib
     return lib
 
@@ -119,6 +124,25 @@ def hq_measures(h, pi, workload, dispatch, stream=None):
     if st != HQ_OK:
         raise HQError(st, lib.hq_error_string(ctypes.c_void_p(h)).decode())
     return loss.value
+
+
+def hq_set_buffer(h, C):
+    """hq_set_buffer(h, C): waiting room of C calls (HQ_BUFFER_UNLIMITED: unlimited)."""
+    lib = load()
+    st = lib.hq_set_buffer(ctypes.c_void_p(h), int(C))
+    if st != HQ_OK:
+        raise HQError(st, lib.hq_error_string(ctypes.c_void_p(h)).decode())
+
+
+def hq_queue_tail(h, n):
+    """(P~{1..n} as a numpy array, sum_c P~{c}) of the last solve."""
+    lib = load()
+    tail = np.zeros(max(int(n), 1))
+    mass = ctypes.c_double(0.0)
+    st = lib.hq_queue_tail(ctypes.c_void_p(h), tail.ctypes.data_as(_dptr), int(n), ctypes.byref(mass))
+    if st != HQ_OK:
+        raise HQError(st, lib.hq_error_string(ctypes.c_void_p(h)).decode())
+    return tail[: int(n)], mass.value
 
 
 def hq_destroy(h):
@@ -177,6 +201,12 @@ class Solver:
             pi = torch.empty(1 << self.N, dtype=torch.float64, device="cuda")
         st, it, res = hq_solve(self.h, tol, max_iter, pi, stream)
         return dict(pi=pi, status=st, iters=it, residual=res)
+
+    def set_buffer(self, C):
+        hq_set_buffer(self.h, C)
+
+    def queue_tail(self, n):
+        return hq_queue_tail(self.h, n)
 
     def measures(self, pi, stream=None):
         import torch

@@ -102,3 +102,23 @@ def test_solve_without_gpu_fails_loudly(hq):
     assert st == hq.HQ_E_CUDA
     assert "CUDA" in hq.hq_error_string(h) or "device" in hq.hq_error_string(h)
     hq.hq_destroy(h)
+
+
+def test_set_buffer_validation(hq):
+    """hq_set_buffer: C >= HQ_BUFFER_UNLIMITED; a waiting room needs full lists; the
+    tail cannot be read before a solve (no compute call is made)."""
+    d = _ok_instance()
+    h = hq.hq_create(d["N"], d["J"], d["lam"], d["mu"], d["pref"])
+    hq.hq_set_buffer(h, 5)
+    hq.hq_set_buffer(h, hq.HQ_BUFFER_UNLIMITED)
+    hq.hq_set_buffer(h, 0)
+    with pytest.raises(hq.HQError, match="HQ_E_INVAL"):
+        hq.hq_set_buffer(h, -2)
+    with pytest.raises(hq.HQError, match="HQ_E_ORDER"):
+        hq.hq_queue_tail(h, 3)
+    hq.hq_destroy(h)
+    t = hq.hq_create(3, 2, [1.0, 0.5], [1.0, 2.0, 0.5], [[0, 1, -1], [2, 1, 0]])
+    with pytest.raises(hq.HQError, match="full preference lists"):
+        hq.hq_set_buffer(t, 3)
+    hq.hq_set_buffer(t, 0)
+    hq.hq_destroy(t)
