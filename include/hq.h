@@ -158,6 +158,34 @@ hq_status hq_set_buffer(hq_handle h, int C);
  */
 hq_status hq_queue_tail(hq_handle h, double *tail, int len, double *mass);
 
+/*
+ * hq_batch_solve -- many small instances in one call:
+ * the paper's usage pattern of load sweeps (9 values per N)
+ * and configuration screening (thousands of N = 9-11 solves).
+ * One CTA per instance with its whole state space in shared memory; Algorithm 1
+ * literally: layers 1..N-1 in order within a sweep, Eq.
+ * updateHeter with the inner normalisation limit (R1), Eqs.
+ * lambdaHeter / muHeter after each layer, Eq. bnd_stationary for p(n); the
+ * relative balance residual r(pi) (R3) every 4 sweeps; stop at r <= tol.
+ *
+ *   B, N, J   instances, units (1 <= N <= 12), atoms (pad with lambda = 0 atoms
+ *             to a common J).
+ *   lambda    [B][J] host, mu [B][N] host, pref [B][J][N] host (int32, -1
+ *             padded rows allowed), each instance validated as in hq_create.
+ *   tol, max_iter  as in hq_solve (max_iter >= 1).
+ *   pi        [B][2^N] DEVICE fp64, caller-owned: pi[b*2^N + m] = P{B_m}.
+ *   cuda_stream    stream to run on; the call synchronises it.
+ *   iters_out, residual_out, status_out  [B] host (may be NULL): sweeps, true
+ *             r(pi) of the returned pi, HQ_OK / HQ_NOT_CONVERGED / HQ_E_NUMERIC.
+ * Returns the worst per-instance status, or HQ_E_INVAL / HQ_E_CUDA (message via
+ * hq_batch_error_string).  Scratch (B * 2^N * N fp64 dispatch rates) is
+ * allocated and freed inside the call.
+ */
+hq_status hq_batch_solve(int B, int N, int J, const double *lambda, const double *mu, const int32_t *pref,
+                         double tol, int max_iter, double *pi, void *cuda_stream, int *iters_out,
+                         double *residual_out, int *status_out);
+const char *hq_batch_error_string(void);
+
 /* Release every device and host resource of h (NULL is a no-op). */
 void hq_destroy(hq_handle h);
 

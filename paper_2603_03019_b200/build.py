@@ -8,7 +8,7 @@ import subprocess
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 LIB = os.path.join(PKG, "libhq.so")
-SOURCES = [os.path.join(PKG, "csrc", n) for n in ("hq_api.cu", "hq_kernels.cu", "hq_v2.cu", "hq_v3.cu")]
+SOURCES = [os.path.join(PKG, "csrc", n) for n in ("hq_api.cu", "hq_kernels.cu", "hq_v2.cu", "hq_v3.cu", "hq_batch.cu")]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",

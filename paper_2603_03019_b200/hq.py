@@ -25,7 +25,7 @@ HQ_STATS_LEN = 20
 STATUS_NAMES = {0: "HQ_OK", 1: "HQ_NOT_CONVERGED", -1: "HQ_E_INVAL", -2: "HQ_E_NOMEM", -3: "HQ_E_CUDA",
                 -4: "HQ_E_NUMERIC", -5: "HQ_E_ORDER"}
 EXPORTED = ["hq_create", "hq_solve", "hq_measures", "hq_destroy", "hq_error_string", "hq_stats", "hq_version",
-            "hq_debug_copy", "hq_set_buffer", "hq_queue_tail"]
+            "hq_debug_copy", "hq_set_buffer", "hq_queue_tail", "hq_batch_solve", "hq_batch_error_string"]
 HQ_BUFFER_UNLIMITED = -1
 
 _dptr = ctypes.POINTER(ctypes.c_double)
@@ -70,6 +70,13 @@ def load():
     lib.hq_set_buffer.argtypes = [ctypes.c_void_p, ctypes.c_int]
     lib.hq_queue_tail.restype = ctypes.c_int
     lib.hq_queue_tail.argtypes = [ctypes.c_void_p, _dptr, ctypes.c_int, _dptr]
+    lib.hq_batch_solve.restype = ctypes.c_int
+    lib.hq_batch_solve.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _dptr, _dptr,
+                                   ctypes.POINTER(ctypes.c_int32), ctypes.c_double, ctypes.c_int, ctypes.c_void_p,
+                                   ctypes.c_void_p, ctypes.POINTER(ctypes.c_int), _dptr,
+                                   ctypes.POINTER(ctypes.c_int)]
+    lib.hq_batch_error_string.restype = ctypes.c_char_p
+    lib.hq_batch_error_string.argtypes = []
     _lib = lib
     return lib
 
@@ -143,6 +150,36 @@ def hq_queue_tail(h, n):
     if st != HQ_OK:
         raise HQError(st, lib.hq_error_string(ctypes.c_void_p(h)).decode())
     return tail[: int(n)], mass.value
+
+
+def hq_batch_solve(lam, mu, pref, tol=1e-13, max_iter=10000, pi=None, stream=None):
+    """hq_batch_solve on stacked instances: lam [B][J], mu [B][N], pref [B][J][N].
+    Returns (pi [B][2^N] CUDA float64 tensor, iters[B], residual[B], status[B]);
+    raises on HQ_E_INVAL / HQ_E_CUDA."""
+    import torch
+
+    lib = load()
+    lam = np.ascontiguousarray(lam, dtype=np.float64)
+    mu = np.ascontiguousarray(mu, dtype=np.float64)
+    pref = np.ascontiguousarray(pref, dtype=np.int32)
+    B, J = lam.shape
+    N = mu.shape[1]
+    if mu.shape != (B, N) or pref.shape != (B, J, N):
+        raise HQError(HQ_E_INVAL, "dimension mismatch")
+    if pi is None:
+        pi = torch.empty((B, 1 << N), dtype=torch.float64, device="cuda")
+    _check_tensor(pi)
+    it = np.zeros(B, dtype=np.int32)
+    res = np.zeros(B)
+    sts = np.zeros(B, dtype=np.int32)
+    st = lib.hq_batch_solve(B, N, J, lam.ctypes.data_as(_dptr), mu.ctypes.data_as(_dptr),
+                            pref.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), float(tol), int(max_iter),
+                            ctypes.c_void_p(pi.data_ptr()), _stream_ptr(stream),
+                            it.ctypes.data_as(ctypes.POINTER(ctypes.c_int)), res.ctypes.data_as(_dptr),
+                            sts.ctypes.data_as(ctypes.POINTER(ctypes.c_int)))
+    if st in (HQ_E_INVAL, HQ_E_CUDA, HQ_E_NOMEM):
+        raise HQError(st, lib.hq_batch_error_string().decode())
+    return pi, it, res, sts
 
 
 def hq_destroy(h):

@@ -122,3 +122,40 @@ def test_set_buffer_validation(hq):
         hq.hq_set_buffer(t, 3)
     hq.hq_set_buffer(t, 0)
     hq.hq_destroy(t)
+
+
+def test_batch_solve_validation(hq):
+    """hq_batch_solve validates every instance before touching the device."""
+    import ctypes
+
+    lib = hq.load()
+    lam = np.array([[1.0, 0.5], [0.0, 0.0]])
+    mu = np.array([[1.0, 2.0, 0.5], [1.0, 1.0, 1.0]])
+    pref = np.array([[[0, 1, 2], [2, 1, 0]]] * 2, dtype=np.int32)
+    dp = ctypes.POINTER(ctypes.c_double)
+    st = lib.hq_batch_solve(2, 3, 2, lam.ctypes.data_as(dp), mu.ctypes.data_as(dp),
+                            pref.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), 1e-13, 100, ctypes.c_void_p(16),
+                            None, None, None, None)
+    assert st == hq.HQ_E_INVAL
+    assert "instance 1" in lib.hq_batch_error_string().decode()
+    st = lib.hq_batch_solve(1, 13, 2, lam.ctypes.data_as(dp), mu.ctypes.data_as(dp),
+                            pref.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), 1e-13, 100, ctypes.c_void_p(16),
+                            None, None, None, None)
+    assert st == hq.HQ_E_INVAL
+
+
+def test_batch_solve_without_gpu_fails_loudly(hq):
+    import ctypes
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    lib = hq.load()
+    lam = np.array([[1.0, 0.5]])
+    mu = np.array([[1.0, 2.0, 0.5]])
+    pref = np.array([[[0, 1, 2], [2, 1, 0]]], dtype=np.int32)
+    dp = ctypes.POINTER(ctypes.c_double)
+    st = lib.hq_batch_solve(1, 3, 2, lam.ctypes.data_as(dp), mu.ctypes.data_as(dp),
+                            pref.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), 1e-13, 100, ctypes.c_void_p(16),
+                            None, None, None, None)
+    assert st == hq.HQ_E_CUDA
