@@ -117,6 +117,28 @@ hq_status hq_measures(hq_handle h, const double *pi, double *workload, double *d
                       void *cuda_stream);
 
 /*
+ * hq_response_times -- response-time measures (SURVEY.md
+ * §8(f) row f3) of the zero-capacity system from the dispatch fractions of
+ * hq_measures:
+ *   MRT   = sum_ij rho_ij tau_ij            MRT_j = sum_i rho_ij tau_ij / sum_i rho_ij
+ *   F(T)  = sum_j f_j P{E(j, T)} / (1 - Pi) F_j(T) = P{E(j, T)} / (1 - Pi)
+ * where E(j, T) = union_i {m in S_ij : tau_ij < T} (strict), so
+ * F(T) = sum_{ij: tau_ij < T} rho_ij and F_j(T) = sum_{i: tau_ij < T} rho_ij / f_j.
+ *
+ *   dispatch  [J*N] DEVICE: rho_ij as written by hq_measures on this handle.
+ *   tau       [J*N] host, row-major [j][i]: response time of unit i to atom j
+ *             (finite, >= 0; units of the caller's choice).
+ *   T_bar     threshold T.
+ *   mrt, frac_within  host scalars: MRT and F(T_bar).
+ *   mrt_j, frac_within_j  [J] DEVICE or NULL: MRT_j and F_j(T_bar) (0 for an atom
+ *             with f_j = 0).
+ * Errors: HQ_E_INVAL (NULL, NaN, negative tau, or a waiting room is set: the paper
+ * defines these measures for C = 0), HQ_E_NOMEM, HQ_E_CUDA.
+ */
+hq_status hq_response_times(hq_handle h, const double *dispatch, const double *tau, double T_bar, double *mrt,
+                            double *frac_within, double *mrt_j, double *frac_within_j, void *cuda_stream);
+
+/*
  * hq_set_buffer -- give calls that find every unit busy a waiting room
  * (SURVEY.md §8(f) row f1).
  *

@@ -39,6 +39,8 @@ cudaError_t zeta(int N, double *g, int grid, cudaStream_t s);
 cudaError_t measures(int N, int J, const double *lam, double Lam, const int32_t *pref, const double *g,
                      double *workload, double *dispatch, double *loss, cudaStream_t s);
 cudaError_t scale(double *x, uint64_t n, double f, int grid, cudaStream_t s);
+cudaError_t response(int N, int J, const double *lam, double Lam, const double *disp, const double *tau, double T,
+                     double *mrt_j, double *f_j, double *tot, cudaStream_t s);
 cudaError_t buffer_measures(int N, int J, const double *lam, double Lam, const double *nu, const double *pi_all_busy,
                             const double *loss_dev, double tail_mass, double tail_last, double loss_q,
                             double *workload, double *dispatch, cudaStream_t s);
@@ -1606,6 +1608,51 @@ extern "C" hq_status hq_solve(hq_handle h, double tol, int max_iter, double *pi,
         }
     }
     return st;
+}
+
+extern "C" hq_status hq_response_times(hq_handle h, const double *dispatch, const double *tau, double T_bar,
+                                       double *mrt, double *frac_within, double *mrt_j, double *frac_within_j,
+                                       void *cuda_stream) {
+    if (!h) return HQ_E_INVAL;
+    if (!dispatch || !tau || !mrt || !frac_within || !(T_bar == T_bar)) {
+        h->err = "NULL argument or NaN threshold";
+        return HQ_E_INVAL;
+    }
+    if (h->bufC != 0) {
+        h->err = "response-time measures are defined for the zero-capacity system (PAPER.md:1015)";
+        return HQ_E_INVAL;
+    }
+    const size_t JN = (size_t)h->J * h->N;
+    for (size_t k = 0; k < JN; k++)
+        if (!std::isfinite(tau[k]) || tau[k] < 0.0) {
+            h->err = "tau must be finite and >= 0";
+            return HQ_E_INVAL;
+        }
+    hq_status st = ensure_device(h);
+    if (st != HQ_OK) return st;
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    double *d_tau = nullptr, *d_tot = nullptr;
+    if (cudaMalloc((void **)&d_tau, sizeof(double) * JN) != cudaSuccess ||
+        cudaMalloc((void **)&d_tot, sizeof(double) * 2) != cudaSuccess) {
+        cudaFree(d_tau);
+        h->err = "device memory for tau could not be allocated";
+        return HQ_E_NOMEM;
+    }
+    double tot[2] = {0.0, 0.0};
+    cudaError_t e = cudaMemcpyAsync(d_tau, tau, sizeof(double) * JN, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess)
+        e = hqk_launch::response(h->N, h->J, h->d_lam, h->Lam, dispatch, d_tau, T_bar, mrt_j, frac_within_j, d_tot, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(tot, d_tot, sizeof(tot), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    cudaFree(d_tau);
+    cudaFree(d_tot);
+    if (e != cudaSuccess) {
+        h->err = std::string("CUDA error: ") + cudaGetErrorString(e);
+        return HQ_E_CUDA;
+    }
+    *mrt = tot[0];
+    *frac_within = tot[1];
+    return HQ_OK;
 }
 
 extern "C" hq_status hq_set_buffer(hq_handle h, int C) {

@@ -437,6 +437,44 @@ __global__ void k_buffer_measures(int N, int J, const double *__restrict__ lam, 
         for (int i = threadIdx.x; i < N; i += blockDim.x) workload[i] += tail_mass;
 }
 
+// Response-time measures from the dispatch
+// fractions rho_ij of k_measures: one CTA, atoms over threads, fixed-order sums.
+//   MRT_j = sum_i rho_ij tau_ij / sum_i rho_ij,  F_j(T) = sum_{i: tau_ij < T} rho_ij / f_j
+//   MRT   = sum_ij rho_ij tau_ij,                F(T)   = sum_{ij: tau_ij < T} rho_ij
+// (E(j, T) is the disjoint union of the S_ij with tau_ij < T, so its mass is sum rho_ij (1 - Pi) / f_j.)
+__global__ void k_response(int N, int J, const double *__restrict__ lam, double Lam, const double *__restrict__ disp,
+                           const double *__restrict__ tau, double T, double *__restrict__ mrt_j,
+                           double *__restrict__ f_j, double *__restrict__ tot) {
+    __shared__ double s_m[1024], s_f[1024];
+    double pm = 0.0, pf = 0.0;
+    for (int j = threadIdx.x; j < J; j += blockDim.x) {
+        double num = 0.0, den = 0.0, fin = 0.0;
+        for (int i = 0; i < N; i++) {
+            const double r = disp[(size_t)j * N + i], t = tau[(size_t)j * N + i];
+            num += r * t;
+            den += r;
+            if (t < T) fin += r;
+        }
+        const double f = lam[j] / Lam;
+        if (mrt_j) mrt_j[j] = den > 0.0 ? num / den : 0.0;
+        if (f_j) f_j[j] = f > 0.0 ? fin / f : 0.0;
+        pm += num;
+        pf += fin;
+    }
+    s_m[threadIdx.x] = pm;
+    s_f[threadIdx.x] = pf;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0.0, b = 0.0;
+        for (int k = 0; k < (int)blockDim.x; k++) {
+            a += s_m[k];
+            b += s_f[k];
+        }
+        tot[0] = a;
+        tot[1] = b;
+    }
+}
+
 }  // namespace hqk
 
 // ---------------------------------------------------------------------------
@@ -485,6 +523,11 @@ cudaError_t zeta(int N, double *g, int grid, cudaStream_t s) {
         if (e != cudaSuccess) return e;
     }
     return cudaSuccess;
+}
+cudaError_t response(int N, int J, const double *lam, double Lam, const double *disp, const double *tau, double T,
+                     double *mrt_j, double *f_j, double *tot, cudaStream_t s) {
+    hqk::k_response<<<1, 1024, 0, s>>>(N, J, lam, Lam, disp, tau, T, mrt_j, f_j, tot);
+    return cudaGetLastError();
 }
 cudaError_t scale(double *x, uint64_t n, double f, int grid, cudaStream_t s) {
     hqk::k_scale<<<grid, 256, 0, s>>>(x, n, f);

@@ -25,7 +25,7 @@ HQ_STATS_LEN = 20
 STATUS_NAMES = {0: "HQ_OK", 1: "HQ_NOT_CONVERGED", -1: "HQ_E_INVAL", -2: "HQ_E_NOMEM", -3: "HQ_E_CUDA",
                 -4: "HQ_E_NUMERIC", -5: "HQ_E_ORDER"}
 EXPORTED = ["hq_create", "hq_solve", "hq_measures", "hq_destroy", "hq_error_string", "hq_stats", "hq_version",
-            "hq_debug_copy", "hq_set_buffer", "hq_queue_tail", "hq_batch_solve", "hq_batch_error_string"]
+            "hq_debug_copy", "hq_set_buffer", "hq_queue_tail", "hq_batch_solve", "hq_batch_error_string", "hq_response_times"]
 HQ_BUFFER_UNLIMITED = -1
 
 _dptr = ctypes.POINTER(ctypes.c_double)
@@ -75,6 +75,9 @@ def load():
                                    ctypes.POINTER(ctypes.c_int32), ctypes.c_double, ctypes.c_int, ctypes.c_void_p,
                                    ctypes.c_void_p, ctypes.POINTER(ctypes.c_int), _dptr,
                                    ctypes.POINTER(ctypes.c_int)]
+    lib.hq_response_times.restype = ctypes.c_int
+    lib.hq_response_times.argtypes = [ctypes.c_void_p, ctypes.c_void_p, _dptr, ctypes.c_double, _dptr, _dptr,
+                                      ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
     lib.hq_batch_error_string.restype = ctypes.c_char_p
     lib.hq_batch_error_string.argtypes = []
     _lib = lib
@@ -182,6 +185,25 @@ def hq_batch_solve(lam, mu, pref, tol=1e-13, max_iter=10000, pi=None, stream=Non
     return pi, it, res, sts
 
 
+def hq_response_times(h, dispatch, tau, T_bar, mrt_j=None, f_j=None, stream=None):
+    """(MRT, F(T_bar)); fills the optional CUDA tensors mrt_j[J], f_j[J]."""
+    lib = load()
+    _check_tensor(dispatch)
+    tau = np.ascontiguousarray(tau, dtype=np.float64)
+    mrt = ctypes.c_double(0.0)
+    frac = ctypes.c_double(0.0)
+    ptr = lambda t: ctypes.c_void_p(t.data_ptr()) if t is not None else None  # noqa: E731
+    for t in (mrt_j, f_j):
+        if t is not None:
+            _check_tensor(t)
+    st = lib.hq_response_times(ctypes.c_void_p(h), ctypes.c_void_p(dispatch.data_ptr()), tau.ctypes.data_as(_dptr),
+                               float(T_bar), ctypes.byref(mrt), ctypes.byref(frac), ptr(mrt_j), ptr(f_j),
+                               _stream_ptr(stream))
+    if st != HQ_OK:
+        raise HQError(st, lib.hq_error_string(ctypes.c_void_p(h)).decode())
+    return mrt.value, frac.value
+
+
 def hq_destroy(h):
     if h:
         load().hq_destroy(ctypes.c_void_p(h))
@@ -238,6 +260,14 @@ class Solver:
             pi = torch.empty(1 << self.N, dtype=torch.float64, device="cuda")
         st, it, res = hq_solve(self.h, tol, max_iter, pi, stream)
         return dict(pi=pi, status=st, iters=it, residual=res)
+
+    def response_times(self, dispatch, tau, T_bar, stream=None):
+        import torch
+
+        mj = torch.empty(self.J, dtype=torch.float64, device=dispatch.device)
+        fj = torch.empty(self.J, dtype=torch.float64, device=dispatch.device)
+        mrt, f = hq_response_times(self.h, dispatch.contiguous(), tau, T_bar, mj, fj, stream)
+        return dict(mrt=mrt, frac_within=f, mrt_j=mj, frac_within_j=fj)
 
     def set_buffer(self, C):
         hq_set_buffer(self.h, C)
