@@ -825,12 +825,18 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
 constexpr int MAXP = V3_MAXPAIRS;   // distinct (unit, pattern) pairs of one program
 constexpr uint32_t PRMASK = 1u | (1u << 1) | (1u << 7) | (1u << 8);   // parity + register units
 
+constexpr int HSLOTS = 2 * MAXP;   // open-addressing index over the keys (load factor <= 1/2)
 struct PairAcc3 {
     int n;
-    uint32_t key[MAXP];   // unit | S << 6
-    double val[MAXP];
+    uint32_t key[MAXP];   // unit | S << 6, in order of first occurrence in the trie walk
+    double val[MAXP];     // sum of the contributions, accumulated in walk order
     uint16_t rm[MAXP];
+    uint16_t hpos[MAXP];  // the key's slot in `slot` (cleared after the program)
+    uint16_t slot[HSLOTS];   // 0: empty, else pair index + 1
 };
+
+__device__ __forceinline__ uint32_t key_hash(uint32_t key) { return (key * 2654435761u) >> (32 - 12); }
+static_assert(HSLOTS == 1 << 12, "key_hash assumes 2^12 slots");
 
 __device__ __forceinline__ bool pair_add3(PairAcc3 &P, double *W0, int u, uint32_t S, double val) {
     if (S == 0u) {
@@ -838,16 +844,26 @@ __device__ __forceinline__ bool pair_add3(PairAcc3 &P, double *W0, int u, uint32
         return true;
     }
     const uint32_t key = (uint32_t)u | (S << 6);
-    for (int i = 0; i < P.n; i++)
+    uint32_t h = key_hash(key);
+    while (P.slot[h]) {
+        const int i = P.slot[h] - 1;
         if (P.key[i] == key) {
             P.val[i] += val;
             return true;
         }
+        h = (h + 1) & (HSLOTS - 1);
+    }
     if (P.n >= MAXP) return false;
+    P.slot[h] = (uint16_t)(P.n + 1);
+    P.hpos[P.n] = (uint16_t)h;
     P.key[P.n] = key;
     P.val[P.n] = val;
     P.n++;
     return true;
+}
+__device__ __forceinline__ void pair_reset3(PairAcc3 &P) {
+    for (int i = 0; i < P.n; i++) P.slot[P.hpos[i]] = 0;
+    P.n = 0;
 }
 
 // admissible register states of a register-dependent pair (unit u, pattern S), beta = 0 | 1 << 8
@@ -892,7 +908,7 @@ __device__ int tile_program(const P3Args &a, uint32_t t, double *W0, PairAcc3 &P
     uint32_t Sst[HQ_MAXN + 2];
     Sst[0] = 0;
     for (int u = 0; u <= HQ_MAXN; u++) W0[u] = 0.0;
-    P.n = 0;
+    pair_reset3(P);
     int v = 0;
     while (v < a.nnodes) {
         const int2 nd = __ldg(&a.node[v]);
@@ -913,6 +929,7 @@ __device__ int tile_program(const P3Args &a, uint32_t t, double *W0, PairAcc3 &P
         v++;
     }
     for (int k = 0; k < P.n; k++) {
+        P.slot[P.hpos[k]] = 0;   // the index is not needed past the walk: leave the table clean
         const int u = (int)(P.key[k] & 63);
         const uint32_t S = P.key[k] >> 6;
         P.rm[k] = (S & PRMASK) ? (uint16_t)reg_mask(u, S, u == a.N) : (uint16_t)0;
@@ -958,6 +975,8 @@ __device__ int tile_program(const P3Args &a, uint32_t t, double *W0, PairAcc3 &P
 __global__ void k_prog_count3(P3Args a, const uint32_t *__restrict__ order, uint32_t *__restrict__ size16,
                               int *__restrict__ err) {
     PairAcc3 P;
+    P.n = 0;
+    for (int h = 0; h < HSLOTS; h++) P.slot[h] = 0;
     double W0[HQ_MAXN + 1];
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.ntiles;
          i += (uint64_t)gridDim.x * blockDim.x) {
@@ -981,6 +1000,8 @@ __device__ __forceinline__ uint32_t pdep9(uint32_t idx, uint32_t M) {   // depos
 __global__ void k_prog_write3(P3Args a, const uint32_t *__restrict__ order, const uint32_t *__restrict__ off16,
                               uint4 *__restrict__ prog, int *__restrict__ err) {
     PairAcc3 P;
+    P.n = 0;
+    for (int h = 0; h < HSLOTS; h++) P.slot[h] = 0;
     double W0[HQ_MAXN + 1];
     const int NVU = 9 + a.nwv;      // units varying inside the program
     const int NT = 9 + a.nW;        // first tile unit (mu_F: busy tile units only)
