@@ -833,6 +833,9 @@ struct PairAcc3 {
     uint16_t rm[MAXP];
     uint16_t hpos[MAXP];  // the key's slot in `slot` (cleared after the program)
     uint16_t slot[HSLOTS];   // 0: empty, else pair index + 1
+    uint32_t tkey[MAXP];  // sort scratch
+    double tval[MAXP];
+    uint16_t trm[MAXP];
 };
 
 __device__ __forceinline__ uint32_t key_hash(uint32_t key) { return (key * 2654435761u) >> (32 - 12); }
@@ -934,25 +937,48 @@ __device__ int tile_program(const P3Args &a, uint32_t t, double *W0, PairAcc3 &P
         const uint32_t S = P.key[k] >> 6;
         P.rm[k] = (S & PRMASK) ? (uint16_t)reg_mask(u, S, u == a.N) : (uint16_t)0;
     }
-    // stable insertion sort by (unit, class, rm); lane-only pairs have rm = 0
-    auto rank = [&](int k) -> uint64_t {
-        return ((uint64_t)(P.key[k] & 63) << 20) | ((uint64_t)(P.rm[k] ? 1 : 0) << 16) | P.rm[k];
-    };
-    for (int x = 1; x < P.n; x++) {
-        const uint32_t kx = P.key[x];
-        const double vx = P.val[x];
-        const uint16_t mx = P.rm[x];
-        const uint64_t rx = rank(x);
-        int y = x - 1;
-        while (y >= 0 && rank(y) > rx) {
-            P.key[y + 1] = P.key[y];
-            P.val[y + 1] = P.val[y];
-            P.rm[y + 1] = P.rm[y];
-            y--;
+    // stable sort by (unit, class, rm); lane-only pairs have rm = 0: a counting sort by unit,
+    // then an insertion sort by (class, rm) inside each unit's (short) run
+    {
+        int cnt[34];
+        for (int u = 0; u < 34; u++) cnt[u] = 0;
+        for (int k = 0; k < P.n; k++) cnt[(P.key[k] & 63) + 1]++;
+        for (int u = 1; u < 34; u++) cnt[u] += cnt[u - 1];
+        for (int k = 0; k < P.n; k++) {
+            const int d = cnt[P.key[k] & 63]++;
+            P.tkey[d] = P.key[k];
+            P.tval[d] = P.val[k];
+            P.trm[d] = P.rm[k];
         }
-        P.key[y + 1] = kx;
-        P.val[y + 1] = vx;
-        P.rm[y + 1] = mx;
+        auto minor = [&](int k) -> uint32_t { return ((uint32_t)(P.trm[k] ? 1 : 0) << 16) | P.trm[k]; };
+        int b0 = 0;
+        while (b0 < P.n) {
+            const uint32_t u = P.tkey[b0] & 63;
+            int b1 = b0 + 1;
+            while (b1 < P.n && (P.tkey[b1] & 63) == u) b1++;
+            for (int x = b0 + 1; x < b1; x++) {
+                const uint32_t kx = P.tkey[x];
+                const double vx = P.tval[x];
+                const uint16_t mx = P.trm[x];
+                const uint32_t rx = minor(x);
+                int y = x - 1;
+                while (y >= b0 && minor(y) > rx) {
+                    P.tkey[y + 1] = P.tkey[y];
+                    P.tval[y + 1] = P.tval[y];
+                    P.trm[y + 1] = P.trm[y];
+                    y--;
+                }
+                P.tkey[y + 1] = kx;
+                P.tval[y + 1] = vx;
+                P.trm[y + 1] = mx;
+            }
+            b0 = b1;
+        }
+        for (int k = 0; k < P.n; k++) {
+            P.key[k] = P.tkey[k];
+            P.val[k] = P.tval[k];
+            P.rm[k] = P.trm[k];
+        }
     }
     // records: per unit with data: a table if it has thread-conditioned pairs, then one
     // group per distinct rm; a table over the lane/warp bits M its conditions use has
