@@ -27,6 +27,59 @@
 #include "hq_v2.h"
 #include "hq_v3.h"
 
+// ---- device memory: the CUDA default memory pool (stream-ordered allocator), so that the
+// working set of a handle is recycled across handles without page (un)mapping; blocks above
+// the release threshold go back to the driver at the next synchronisation.  dfree keeps
+// cudaFree's device-wide synchronisation (nothing may still use the block).
+static void pool_init() {
+    static std::once_flag once;
+    std::call_once(once, [] {
+        int dev = 0;
+        cudaMemPool_t pool;
+        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = 8ull << 30;   // keep up to 8 GB cached between handles
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        cudaGetLastError();
+    });
+}
+static cudaError_t dmalloc(void **p, size_t bytes) {
+    pool_init();
+    cudaError_t e = cudaMallocAsync(p, bytes ? bytes : 16, 0);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(0);   // usable from any stream on return
+    if (e != cudaSuccess) {
+        *p = nullptr;
+        cudaGetLastError();
+    }
+    return e;
+}
+static void dfree(void *p) {
+    if (!p) return;
+    cudaDeviceSynchronize();
+    cudaFreeAsync(p, 0);
+}
+// small pinned host buffers, recycled across handles (cudaMallocHost / cudaFreeHost are slow)
+static std::mutex g_pin_mu;
+static std::vector<std::pair<size_t, void *>> g_pin_free;
+static cudaError_t pinned_alloc(void **p, size_t bytes) {
+    {
+        std::lock_guard<std::mutex> lk(g_pin_mu);
+        for (size_t i = 0; i < g_pin_free.size(); i++)
+            if (g_pin_free[i].first == bytes) {
+                *p = g_pin_free[i].second;
+                g_pin_free.erase(g_pin_free.begin() + (long)i);
+                return cudaSuccess;
+            }
+    }
+    return cudaMallocHost(p, bytes);
+}
+static void pinned_free(void *p, size_t bytes) {
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    if (g_pin_free.size() < 64) g_pin_free.emplace_back(bytes, p);
+    else cudaFreeHost(p);
+}
+
 namespace hqk_launch {
 cudaError_t gather(const KArgs &k, int grid, cudaStream_t s);
 cudaError_t finalize(const KArgs &k, int grid, cudaStream_t s);
@@ -282,6 +335,8 @@ std::vector<int> choose_perm_v3(int N, const TrieHost &tr, int nW) {
 }
 }  // namespace
 
+enum { S_LAM = 0, S_MU = 32, S_MUSTAR = 64, S_PN = 96, S_STATS = 128, S_INVC = 256, S_TOTAL = 288 };
+
 struct hq_problem {
     int N = 0, J = 0;
     double Lam = 0.0;
@@ -348,36 +403,36 @@ struct hq_problem {
         for (auto e : ev) cudaEventDestroy(e);
     }
     void release() {
-        cudaFree(d_node);
-        cudaFree(d_lthr);
-        cudaFree(d_lend);
-        cudaFree(d_lam);
-        cudaFree(d_pref);
-        cudaFree(d_pw);
-        cudaFree(d_ab);
-        cudaFree(d_partial);
-        cudaFree(d_small);
-        cudaFree(d_err);
-        cudaFree(d_order);
-        cudaFree(d_range);
+        dfree(d_node);
+        dfree(d_lthr);
+        dfree(d_lend);
+        dfree(d_lam);
+        dfree(d_pref);
+        dfree(d_pw);
+        dfree(d_ab);
+        dfree(d_partial);
+        dfree(d_small);
+        dfree(d_err);
+        dfree(d_order);
+        dfree(d_range);
         d_range = nullptr;
-        cudaFree(d_done);
+        dfree(d_done);
         d_done = nullptr;
-        cudaFree(d_wtime);
+        dfree(d_wtime);
         d_wtime = nullptr;
-        cudaFree(d_off16);
-        cudaFree(d_size16);
-        cudaFree(d_prog);
-        cudaFree(d_omkap);
-        cudaFree(d_lamarr);
-        cudaFree(d_blk);
-        if (h_blk) cudaFreeHost(h_blk);
+        dfree(d_off16);
+        dfree(d_size16);
+        dfree(d_prog);
+        dfree(d_omkap);
+        dfree(d_lamarr);
+        dfree(d_blk);
+        pinned_free(h_blk, sizeof(double) * V2S_TOTAL);
         d_order = d_off16 = d_size16 = nullptr;
         d_prog = nullptr;
         d_omkap = nullptr;
         d_lamarr = d_blk = h_blk = nullptr;
         v2_ready = false;
-        if (h_small) cudaFreeHost(h_small);
+        pinned_free(h_small, sizeof(double) * S_TOTAL);
         d_node = nullptr;
         d_lthr = d_lend = d_lam = nullptr;
         d_pref = nullptr;
@@ -390,7 +445,6 @@ struct hq_problem {
 };
 
 // small-array layout inside d_small / h_small
-enum { S_LAM = 0, S_MU = 32, S_MUSTAR = 64, S_PN = 96, S_STATS = 128, S_INVC = 256, S_TOTAL = 288 };
 
 #define HQ_CUDA(call)                                                                   \
     do {                                                                                \
@@ -497,7 +551,7 @@ static hq_status ensure_device(hq_problem *h) {
     const uint64_t ntiles = ((S >> 1) + hqk_launch::tile_states() - 1) / hqk_launch::tile_states();
     h->grid = (int)std::min<uint64_t>(ntiles, (uint64_t)h->nsm * 4);
     const size_t nn = h->trie.node.size();
-    auto alloc = [&](void **p, size_t bytes) -> cudaError_t { return cudaMalloc(p, bytes ? bytes : 16); };
+    auto alloc = [&](void **p, size_t bytes) -> cudaError_t { return dmalloc(p, bytes ? bytes : 16); };
     if (h->path == 3) {
         const uint64_t nt3 = 1ull << (N - 9 - h->nW);
         h->sgrid = (int)std::min<uint64_t>(nt3, (uint64_t)h->nsm * hq3_launch::ctas_per_sm(h->nW));
@@ -520,10 +574,10 @@ static hq_status ensure_device(hq_problem *h) {
     HQ_CUDA(alloc((void **)&h->d_pref, sizeof(int32_t) * h->J * N));
     HQ_CUDA(alloc((void **)&h->d_partial, sizeof(double) * 2 * std::max(h->grid, h->sgrid) * HQ_NL * HQ_NV));
     HQ_CUDA(alloc((void **)&h->d_blk, sizeof(double) * 2 * V2S_TOTAL));   // [0]: the block, [1]: fold buffer
-    HQ_CUDA(cudaMallocHost((void **)&h->h_blk, sizeof(double) * V2S_TOTAL));
+    HQ_CUDA(pinned_alloc((void **)&h->h_blk, sizeof(double) * V2S_TOTAL));
     HQ_CUDA(alloc((void **)&h->d_small, sizeof(double) * S_TOTAL));
     HQ_CUDA(alloc((void **)&h->d_err, sizeof(int)));
-    HQ_CUDA(cudaMallocHost((void **)&h->h_small, sizeof(double) * S_TOTAL));
+    HQ_CUDA(pinned_alloc((void **)&h->h_small, sizeof(double) * S_TOTAL));
     HQ_CUDA(cudaMemcpy(h->d_node, h->trie.node.data(), sizeof(int2) * nn, cudaMemcpyHostToDevice));
     HQ_CUDA(cudaMemcpy(h->d_lthr, h->trie.lam_thr.data(), sizeof(double) * nn, cudaMemcpyHostToDevice));
     HQ_CUDA(cudaMemcpy(h->d_lend, h->trie.lam_end.data(), sizeof(double) * nn, cudaMemcpyHostToDevice));
@@ -635,7 +689,7 @@ static hq_status v2_prepare(hq_problem *h, cudaStream_t s) {
             for (uint32_t x = 0; x < (1u << nWp); x++) w[(i << nWp) | x] = (order[i] << nWp) | x;
         order.swap(w);
     }
-    auto alloc = [&](void **p, size_t bytes) -> cudaError_t { return cudaMalloc(p, bytes ? bytes : 16); };
+    auto alloc = [&](void **p, size_t bytes) -> cudaError_t { return dmalloc(p, bytes ? bytes : 16); };
     if (alloc((void **)&h->d_order, 4 * nprog) != cudaSuccess || alloc((void **)&h->d_off16, 4 * nprog) != cudaSuccess ||
         alloc((void **)&h->d_size16, 4 * nprog) != cudaSuccess ||
         (!h->full_lists && alloc((void **)&h->d_lamarr, 8 * S) != cudaSuccess)) {
@@ -718,18 +772,18 @@ static hq_status v2_prepare(hq_problem *h, cudaStream_t s) {
             acc += cost[i];
             while (b < G && acc >= tot * b / G) range[b++] = (uint32_t)(i + 1);
         }
-        cudaFree(h->d_range);
+        dfree(h->d_range);
         h->d_range = nullptr;
-        HQ_CUDA(cudaMalloc((void **)&h->d_range, 4 * (G + 1)));
+        HQ_CUDA(dmalloc((void **)&h->d_range, 4 * (G + 1)));
         if (!h->d_done) {
-            HQ_CUDA(cudaMalloc((void **)&h->d_done, sizeof(unsigned)));
+            HQ_CUDA(dmalloc((void **)&h->d_done, sizeof(unsigned)));
             HQ_CUDA(cudaMemset(h->d_done, 0, sizeof(unsigned)));
         }
         HQ_CUDA(cudaMemcpy(h->d_range, range.data(), 4 * (G + 1), cudaMemcpyHostToDevice));
     }
-    cudaFree(tmp);
-    cudaFree(tmp2);
-    cudaFree(d_max);
+    dfree(tmp);
+    dfree(tmp2);
+    dfree(d_max);
     if (h->path == 3) {   // staged program capacity; larger blocks are read from global memory
         h->maxblk_all = h->maxrec;
         h->maxrec = hq3_launch::choose_cap(h->nW, h->maxrec);
@@ -766,7 +820,7 @@ static hq_status v2_prepare(hq_problem *h, cudaStream_t s) {
     cudaEventElapsedTime(&ms, e0, e1);
     h->precompute_ms = ms;
     h->prog_bytes = 16.0 * (double)total16;
-    cudaFree(h->d_size16);
+    dfree(h->d_size16);
     h->d_size16 = nullptr;
     (void)half;
     h->v2_ready = true;
@@ -783,9 +837,9 @@ struct ProgSet {
     uint32_t total16 = 0, maxblk = 0, cap = 0;
     int nwv = 0;
     void release() {
-        cudaFree(off16);
-        cudaFree(range);
-        cudaFree(prog);
+        dfree(off16);
+        dfree(range);
+        dfree(prog);
         off16 = range = nullptr;
         prog = nullptr;
     }
@@ -807,14 +861,14 @@ static hq_status v3_programs(hq_problem *h, cudaStream_t s, int nwv, const std::
     uint32_t *d_pord = nullptr, *d_size = nullptr, *d_offp = nullptr, *d_max = nullptr;
     void *tmp = nullptr;
     auto cleanup = [&]() {
-        cudaFree(d_pord);
-        cudaFree(d_size);
-        cudaFree(d_offp);
-        cudaFree(d_max);
-        cudaFree(tmp);
+        dfree(d_pord);
+        dfree(d_size);
+        dfree(d_offp);
+        dfree(d_max);
+        dfree(tmp);
     };
-    if (cudaMalloc((void **)&d_pord, 4 * nprog) != cudaSuccess || cudaMalloc((void **)&d_size, 4 * nprog) != cudaSuccess ||
-        cudaMalloc((void **)&d_offp, 4 * nprog) != cudaSuccess) {
+    if (dmalloc((void **)&d_pord, 4 * nprog) != cudaSuccess || dmalloc((void **)&d_size, 4 * nprog) != cudaSuccess ||
+        dmalloc((void **)&d_offp, 4 * nprog) != cudaSuccess) {
         cudaGetLastError();
         cleanup();
         h->err = "device memory for the rate-program tables could not be allocated";
@@ -838,7 +892,7 @@ static hq_status v3_programs(hq_problem *h, cudaStream_t s, int nwv, const std::
     HQ_CUDA(hq3_launch::prog_count(p3, d_pord, d_size, h->d_err, g, s));
     size_t tb = 0;
     HQ_CUDA(hq2_launch::prog_scan(d_size, d_offp, nprog, nullptr, &tb, s));
-    HQ_CUDA(cudaMalloc(&tmp, tb ? tb : 16));
+    HQ_CUDA(dmalloc(&tmp, tb ? tb : 16));
     HQ_CUDA(hq2_launch::prog_scan(d_size, d_offp, nprog, tmp, &tb, s));
     std::vector<uint32_t> sz(nprog), offp(nprog);
     int herr = 0;
@@ -860,8 +914,8 @@ static hq_status v3_programs(hq_problem *h, cudaStream_t s, int nwv, const std::
     ps.release();
     ps.nwv = nwv;
     ps.total16 = (uint32_t)total16;
-    if (cudaMalloc((void **)&ps.prog, 16 * (total16 ? total16 : 1)) != cudaSuccess ||
-        cudaMalloc((void **)&ps.off16, 4 * (ntiles << nW)) != cudaSuccess) {
+    if (dmalloc((void **)&ps.prog, 16 * (total16 ? total16 : 1)) != cudaSuccess ||
+        dmalloc((void **)&ps.off16, 4 * (ntiles << nW)) != cudaSuccess) {
         cudaGetLastError();
         cleanup();
         ps.release();
@@ -927,7 +981,7 @@ static hq_status v3_programs(hq_problem *h, cudaStream_t s, int nwv, const std::
         else lo = mid;
     }
     pack(hi, &range);
-    HQ_CUDA(cudaMalloc((void **)&ps.range, 4 * (G + 1)));
+    HQ_CUDA(dmalloc((void **)&ps.range, 4 * (G + 1)));
     HQ_CUDA(cudaMemcpyAsync(ps.range, range.data(), 4 * (G + 1), cudaMemcpyHostToDevice, s));
     HQ_CUDA(cudaMemcpyAsync(&herr, h->d_err, sizeof(int), cudaMemcpyDeviceToHost, s));
     HQ_CUDA(cudaStreamSynchronize(s));
@@ -942,9 +996,9 @@ static hq_status v3_programs(hq_problem *h, cudaStream_t s, int nwv, const std::
 }
 
 static void use_progset(hq_problem *h, ProgSet &ps) {
-    cudaFree(h->d_off16);
-    cudaFree(h->d_range);
-    cudaFree(h->d_prog);
+    dfree(h->d_off16);
+    dfree(h->d_range);
+    dfree(h->d_prog);
     h->d_off16 = ps.off16;
     h->d_range = ps.range;
     h->d_prog = ps.prog;
@@ -1008,8 +1062,8 @@ static hq_status v3_prepare(hq_problem *h, cudaStream_t s) {
             x = (((r ^ x) >> 2) / cc) | r;
         }
     }
-    if (cudaMalloc((void **)&h->d_order, 4 * ntiles) != cudaSuccess ||
-        (!h->full_lists && cudaMalloc((void **)&h->d_lamarr, 8 * S) != cudaSuccess)) {
+    if (dmalloc((void **)&h->d_order, 4 * ntiles) != cudaSuccess ||
+        (!h->full_lists && dmalloc((void **)&h->d_lamarr, 8 * S) != cudaSuccess)) {
         cudaGetLastError();
         h->err = "device memory for the tile tables could not be allocated";
         return HQ_E_NOMEM;
@@ -1031,7 +1085,7 @@ static hq_status v3_prepare(hq_problem *h, cudaStream_t s) {
     if (!h->full_lists) HQ_CUDA(hq2_launch::lambda_states(pa, h->d_lamarr, g, s));
     HQ_CUDA(hq2_launch::omkap(pa, h->d_lamarr, h->d_omkap, g, s));
     if (!h->d_done) {
-        HQ_CUDA(cudaMalloc((void **)&h->d_done, sizeof(unsigned)));
+        HQ_CUDA(dmalloc((void **)&h->d_done, sizeof(unsigned)));
         HQ_CUDA(cudaMemsetAsync(h->d_done, 0, sizeof(unsigned), s));
     }
     // program granularity: warp programs (warp bits folded; fewer pairs per thread; the
@@ -1134,7 +1188,7 @@ static cudaError_t tiled_sweep(hq_problem *h, const S2Args &sa, int mode, cudaSt
     a.full_lists = sa.full_lists;
     a.warp_programs = (h->prog_nwv == 0) ? 1 : 0;
     a.all_staged = h->maxblk_all <= h->maxrec ? 1 : 0;
-    if (!h->d_wtime && cudaMalloc((void **)&h->d_wtime, 8 * 4096) == cudaSuccess) cudaMemset(h->d_wtime, 0, 8 * 4096);
+    if (!h->d_wtime && dmalloc((void **)&h->d_wtime, 8 * 4096) == cudaSuccess) cudaMemset(h->d_wtime, 0, 8 * 4096);
     a.wtime = h->d_wtime;
     a.Q = sa.Q;
     a.P = sa.P;
@@ -1632,9 +1686,9 @@ extern "C" hq_status hq_response_times(hq_handle h, const double *dispatch, cons
     if (st != HQ_OK) return st;
     cudaStream_t s = (cudaStream_t)cuda_stream;
     double *d_tau = nullptr, *d_tot = nullptr;
-    if (cudaMalloc((void **)&d_tau, sizeof(double) * JN) != cudaSuccess ||
-        cudaMalloc((void **)&d_tot, sizeof(double) * 2) != cudaSuccess) {
-        cudaFree(d_tau);
+    if (dmalloc((void **)&d_tau, sizeof(double) * JN) != cudaSuccess ||
+        dmalloc((void **)&d_tot, sizeof(double) * 2) != cudaSuccess) {
+        dfree(d_tau);
         h->err = "device memory for tau could not be allocated";
         return HQ_E_NOMEM;
     }
@@ -1644,8 +1698,8 @@ extern "C" hq_status hq_response_times(hq_handle h, const double *dispatch, cons
         e = hqk_launch::response(h->N, h->J, h->d_lam, h->Lam, dispatch, d_tau, T_bar, mrt_j, frac_within_j, d_tot, s);
     if (e == cudaSuccess) e = cudaMemcpyAsync(tot, d_tot, sizeof(tot), cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    cudaFree(d_tau);
-    cudaFree(d_tot);
+    dfree(d_tau);
+    dfree(d_tot);
     if (e != cudaSuccess) {
         h->err = std::string("CUDA error: ") + cudaGetErrorString(e);
         return HQ_E_CUDA;
