@@ -199,13 +199,17 @@ hq_status hq_queue_tail(hq_handle h, double *tail, int len, double *mass);
  *   cuda_stream    stream to run on; the call synchronises it.
  *   iters_out, residual_out, status_out  [B] host (may be NULL): sweeps, true
  *             r(pi) of the returned pi, HQ_OK / HQ_NOT_CONVERGED / HQ_E_NUMERIC.
+ *   workload  [B][N] DEVICE or NULL, dispatch [B][J][N] DEVICE or NULL,
+ *   loss_out  [B] host or NULL: the measures of hq_measures per instance, computed
+ *             on chip from the instance's pi (superset sums, fixed order).
  * Returns the worst per-instance status, or HQ_E_INVAL / HQ_E_CUDA (message via
  * hq_batch_error_string).  Scratch (B * 2^N * N fp64 dispatch rates) is
  * allocated and freed inside the call.
  */
 hq_status hq_batch_solve(int B, int N, int J, const double *lambda, const double *mu, const int32_t *pref,
                          double tol, int max_iter, double *pi, void *cuda_stream, int *iters_out,
-                         double *residual_out, int *status_out);
+                         double *residual_out, int *status_out, double *workload, double *dispatch,
+                         double *loss_out);
 const char *hq_batch_error_string(void);
 
 /* Release every device and host resource of h (NULL is a no-op). */

@@ -31,7 +31,7 @@
 // working set of a handle is recycled across handles without page (un)mapping; blocks above
 // the release threshold go back to the driver at the next synchronisation.  dfree keeps
 // cudaFree's device-wide synchronisation (nothing may still use the block).
-static void pool_init() {
+void hq_pool_init() {   // also used by hq_batch.cu
     static std::once_flag once;
     std::call_once(once, [] {
         int dev = 0;
@@ -44,7 +44,7 @@ static void pool_init() {
     });
 }
 static cudaError_t dmalloc(void **p, size_t bytes) {
-    pool_init();
+    hq_pool_init();
     cudaError_t e = cudaMallocAsync(p, bytes ? bytes : 16, 0);
     if (e == cudaSuccess) e = cudaStreamSynchronize(0);   // usable from any stream on return
     if (e != cudaSuccess) {

@@ -43,6 +43,9 @@ struct BArgs {
     int *iters;              // [B]
     double *res;             // [B]
     int *err;                // [B] 0 ok, 1 numeric
+    double *workload;        // [B][N] or NULL: rho_i = P(unit i busy)
+    double *dispatch;        // [B][J][N] or NULL: rho_ij
+    double *loss;            // [B] or NULL
 };
 
 __global__ void k_batch_dispatch(BArgs a, double *Wd) {
@@ -216,11 +219,58 @@ __global__ void __launch_bounds__(kThreads) k_batch_solve(BArgs a) {
             a.res[b] = r;
             a.err[b] = bad;
         }
+        if (a.workload || a.dispatch || a.loss) {
+            // measures (as k_measures of the single-instance path): superset sums
+            // g(T) = sum_{m superset of T} pi(m) by an in-place zeta transform (fixed order), then
+            //   rho_i = g({i}),  loss = sum_j f_j g(list_j),
+            //   rho_ij = f_j (g(units before i in zeta_j) - g(units through i)) / (1 - loss)
+            double *g = xs;
+            for (uint32_t m = tid; m < S; m += blockDim.x) g[m] = s_pn[__popc(m)] * p[m];
+            for (int bit = 0; bit < N; bit++) {
+                __syncthreads();
+                for (uint32_t k = tid; k < (S >> 1); k += blockDim.x) {
+                    const uint32_t lo = k & ((1u << bit) - 1u), m = ((k >> bit) << (bit + 1)) | lo;
+                    g[m] += g[m | (1u << bit)];
+                }
+            }
+            __syncthreads();
+            const double *lam = a.lam + (uint64_t)b * a.J;
+            const int32_t *pref = a.pref + (uint64_t)b * a.J * N;
+            double Lam = 0.0;
+            for (int j = 0; j < a.J; j++) Lam += lam[j];
+            double lp = 0.0;   // per-thread part of the loss, atoms tid, tid + blockDim, ...
+            for (int j = tid; j < a.J; j += blockDim.x) {
+                uint32_t T = 0;
+                for (int h = 0; h < N && pref[(uint64_t)j * N + h] >= 0; h++) T |= 1u << pref[(uint64_t)j * N + h];
+                lp += lam[j] / Lam * g[T];
+            }
+            const double2 L = block_sum2(lp, 0.0, scr);
+            const double loss = L.x;
+            if (a.loss && tid == 0) a.loss[b] = loss;
+            if (a.workload)
+                for (int i = tid; i < N; i += blockDim.x) a.workload[(uint64_t)b * N + i] = g[1u << i];
+            if (a.dispatch)
+                for (int j = tid; j < a.J; j += blockDim.x) {
+                    double *row = a.dispatch + ((uint64_t)b * a.J + j) * N;
+                    for (int i = 0; i < N; i++) row[i] = 0.0;
+                    const double f = lam[j] / Lam;
+                    uint32_t T = 0;
+                    for (int h = 0; h < N; h++) {
+                        const int u = pref[(uint64_t)j * N + h];
+                        if (u < 0) break;
+                        const uint32_t T2 = T | (1u << u);
+                        row[u] = f * (g[T] - g[T2]) / (1.0 - loss);
+                        T = T2;
+                    }
+                }
+        }
         __syncthreads();
     }
 }
 
 }  // namespace hqb
+
+void hq_pool_init();   // hq_api.cu: release threshold of the default memory pool
 
 namespace {
 thread_local std::string g_batch_error;
@@ -235,7 +285,8 @@ extern "C" const char *hq_batch_error_string(void) { return g_batch_error.c_str(
 
 extern "C" hq_status hq_batch_solve(int B, int N, int J, const double *lambda, const double *mu, const int32_t *pref,
                                     double tol, int max_iter, double *pi, void *cuda_stream, int *iters_out,
-                                    double *residual_out, int *status_out) {
+                                    double *residual_out, int *status_out, double *workload, double *dispatch,
+                                    double *loss_out) {
     if (B < 1 || N < 1 || N > hqb::kMaxN || J < 1) return batch_fail("need B >= 1, 1 <= N <= 12, J >= 1");
     if (!lambda || !mu || !pref || !pi) return batch_fail("NULL argument");
     if (max_iter < 1 || !(tol == tol)) return batch_fail("max_iter must be >= 1 and tol not NaN");
@@ -275,6 +326,7 @@ extern "C" hq_status hq_batch_solve(int B, int N, int J, const double *lambda, c
             if (!reach[i]) return batch_fail("instance " + std::to_string(b) + ": reducible chain (unit in no list)");
     }
     cudaStream_t s = (cudaStream_t)cuda_stream;
+    hq_pool_init();
     const uint32_t S = 1u << N;
     hqb::BArgs a;
     memset(&a, 0, sizeof(a));
@@ -296,15 +348,17 @@ extern "C" hq_status hq_batch_solve(int B, int N, int J, const double *lambda, c
     int32_t *d_pref = nullptr;
     uint16_t *d_order = nullptr;
     int *d_it = nullptr, *d_err = nullptr;
-    auto cleanup = [&]() {
-        cudaFree(d_lam);
-        cudaFree(d_nu);
-        cudaFree(d_Wd);
-        cudaFree(d_res);
-        cudaFree(d_pref);
-        cudaFree(d_order);
-        cudaFree(d_it);
-        cudaFree(d_err);
+    double *d_loss = nullptr;
+    auto cleanup = [&]() {   // stream-ordered frees (the default pool recycles the blocks)
+        if (d_lam) cudaFreeAsync(d_lam, s);
+        if (d_nu) cudaFreeAsync(d_nu, s);
+        if (d_Wd) cudaFreeAsync(d_Wd, s);
+        if (d_res) cudaFreeAsync(d_res, s);
+        if (d_pref) cudaFreeAsync(d_pref, s);
+        if (d_order) cudaFreeAsync(d_order, s);
+        if (d_it) cudaFreeAsync(d_it, s);
+        if (d_err) cudaFreeAsync(d_err, s);
+        if (d_loss) cudaFreeAsync(d_loss, s);
     };
 #define HQB_CUDA(x)                                                                          \
     do {                                                                                     \
@@ -314,14 +368,14 @@ extern "C" hq_status hq_batch_solve(int B, int N, int J, const double *lambda, c
             return batch_fail(std::string("CUDA error: ") + cudaGetErrorString(e_), HQ_E_CUDA); \
         }                                                                                    \
     } while (0)
-    HQB_CUDA(cudaMalloc((void **)&d_lam, sizeof(double) * B * J));
-    HQB_CUDA(cudaMalloc((void **)&d_nu, sizeof(double) * B * N));
-    HQB_CUDA(cudaMalloc((void **)&d_pref, sizeof(int32_t) * B * J * N));
-    HQB_CUDA(cudaMalloc((void **)&d_Wd, sizeof(double) * (size_t)B * S * N));
-    HQB_CUDA(cudaMalloc((void **)&d_order, sizeof(uint16_t) * S));
-    HQB_CUDA(cudaMalloc((void **)&d_res, sizeof(double) * B));
-    HQB_CUDA(cudaMalloc((void **)&d_it, sizeof(int) * B));
-    HQB_CUDA(cudaMalloc((void **)&d_err, sizeof(int) * B));
+    HQB_CUDA(cudaMallocAsync((void **)&d_lam, sizeof(double) * B * J, s));
+    HQB_CUDA(cudaMallocAsync((void **)&d_nu, sizeof(double) * B * N, s));
+    HQB_CUDA(cudaMallocAsync((void **)&d_pref, sizeof(int32_t) * B * J * N, s));
+    HQB_CUDA(cudaMallocAsync((void **)&d_Wd, sizeof(double) * (size_t)B * S * N, s));
+    HQB_CUDA(cudaMallocAsync((void **)&d_order, sizeof(uint16_t) * S, s));
+    HQB_CUDA(cudaMallocAsync((void **)&d_res, sizeof(double) * B, s));
+    HQB_CUDA(cudaMallocAsync((void **)&d_it, sizeof(int) * B, s));
+    HQB_CUDA(cudaMallocAsync((void **)&d_err, sizeof(int) * B, s));
     HQB_CUDA(cudaMemcpyAsync(d_lam, lambda, sizeof(double) * B * J, cudaMemcpyHostToDevice, s));
     HQB_CUDA(cudaMemcpyAsync(d_nu, mu, sizeof(double) * B * N, cudaMemcpyHostToDevice, s));
     HQB_CUDA(cudaMemcpyAsync(d_pref, pref, sizeof(int32_t) * B * J * N, cudaMemcpyHostToDevice, s));
@@ -335,6 +389,12 @@ extern "C" hq_status hq_batch_solve(int B, int N, int J, const double *lambda, c
     a.iters = d_it;
     a.res = d_res;
     a.err = d_err;
+    a.workload = workload;
+    a.dispatch = dispatch;
+    if (loss_out) {
+        HQB_CUDA(cudaMallocAsync((void **)&d_loss, sizeof(double) * B, s));
+        a.loss = d_loss;
+    }
     int dev = 0, nsm = 148;
     HQB_CUDA(cudaGetDevice(&dev));
     HQB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
@@ -352,6 +412,7 @@ extern "C" hq_status hq_batch_solve(int B, int N, int J, const double *lambda, c
     HQB_CUDA(cudaMemcpyAsync(it.data(), d_it, sizeof(int) * B, cudaMemcpyDeviceToHost, s));
     HQB_CUDA(cudaMemcpyAsync(rr.data(), d_res, sizeof(double) * B, cudaMemcpyDeviceToHost, s));
     HQB_CUDA(cudaMemcpyAsync(er.data(), d_err, sizeof(int) * B, cudaMemcpyDeviceToHost, s));
+    if (loss_out) HQB_CUDA(cudaMemcpyAsync(loss_out, d_loss, sizeof(double) * B, cudaMemcpyDeviceToHost, s));
     HQB_CUDA(cudaStreamSynchronize(s));
     cleanup();
     hq_status worst = HQ_OK;

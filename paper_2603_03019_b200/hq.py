@@ -74,7 +74,7 @@ def load():
     lib.hq_batch_solve.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _dptr, _dptr,
                                    ctypes.POINTER(ctypes.c_int32), ctypes.c_double, ctypes.c_int, ctypes.c_void_p,
                                    ctypes.c_void_p, ctypes.POINTER(ctypes.c_int), _dptr,
-                                   ctypes.POINTER(ctypes.c_int)]
+                                   ctypes.POINTER(ctypes.c_int), ctypes.c_void_p, ctypes.c_void_p, _dptr]
     lib.hq_response_times.restype = ctypes.c_int
     lib.hq_response_times.argtypes = [ctypes.c_void_p, ctypes.c_void_p, _dptr, ctypes.c_double, _dptr, _dptr,
                                       ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
@@ -155,10 +155,11 @@ def hq_queue_tail(h, n):
     return tail[: int(n)], mass.value
 
 
-def hq_batch_solve(lam, mu, pref, tol=1e-13, max_iter=10000, pi=None, stream=None):
+def hq_batch_solve(lam, mu, pref, tol=1e-13, max_iter=10000, pi=None, stream=None, measures=None):
     """hq_batch_solve on stacked instances: lam [B][J], mu [B][N], pref [B][J][N].
-    Returns (pi [B][2^N] CUDA float64 tensor, iters[B], residual[B], status[B]);
-    raises on HQ_E_INVAL / HQ_E_CUDA."""
+    Returns (pi [B][2^N] CUDA float64 tensor, iters[B], residual[B], status[B]); with a
+    dict ``measures`` it is filled with workload [B][N], dispatch [B][J][N] (CUDA) and
+    loss [B] (numpy).  Raises on HQ_E_INVAL / HQ_E_CUDA."""
     import torch
 
     lib = load()
@@ -175,11 +176,20 @@ def hq_batch_solve(lam, mu, pref, tol=1e-13, max_iter=10000, pi=None, stream=Non
     it = np.zeros(B, dtype=np.int32)
     res = np.zeros(B)
     sts = np.zeros(B, dtype=np.int32)
+    w = d = None
+    loss = np.zeros(B)
+    if measures is not None:
+        w = torch.empty((B, N), dtype=torch.float64, device=pi.device)
+        d = torch.empty((B, J, N), dtype=torch.float64, device=pi.device)
+        measures.update(workload=w, dispatch=d, loss=loss)
     st = lib.hq_batch_solve(B, N, J, lam.ctypes.data_as(_dptr), mu.ctypes.data_as(_dptr),
                             pref.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), float(tol), int(max_iter),
                             ctypes.c_void_p(pi.data_ptr()), _stream_ptr(stream),
                             it.ctypes.data_as(ctypes.POINTER(ctypes.c_int)), res.ctypes.data_as(_dptr),
-                            sts.ctypes.data_as(ctypes.POINTER(ctypes.c_int)))
+                            sts.ctypes.data_as(ctypes.POINTER(ctypes.c_int)),
+                            ctypes.c_void_p(w.data_ptr()) if w is not None else None,
+                            ctypes.c_void_p(d.data_ptr()) if d is not None else None,
+                            loss.ctypes.data_as(_dptr) if measures is not None else None)
     if st in (HQ_E_INVAL, HQ_E_CUDA, HQ_E_NOMEM):
         raise HQError(st, lib.hq_batch_error_string().decode())
     return pi, it, res, sts

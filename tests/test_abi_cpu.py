@@ -135,12 +135,12 @@ def test_batch_solve_validation(hq):
     dp = ctypes.POINTER(ctypes.c_double)
     st = lib.hq_batch_solve(2, 3, 2, lam.ctypes.data_as(dp), mu.ctypes.data_as(dp),
                             pref.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), 1e-13, 100, ctypes.c_void_p(16),
-                            None, None, None, None)
+                            None, None, None, None, None, None, None)
     assert st == hq.HQ_E_INVAL
     assert "instance 1" in lib.hq_batch_error_string().decode()
     st = lib.hq_batch_solve(1, 13, 2, lam.ctypes.data_as(dp), mu.ctypes.data_as(dp),
                             pref.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), 1e-13, 100, ctypes.c_void_p(16),
-                            None, None, None, None)
+                            None, None, None, None, None, None, None)
     assert st == hq.HQ_E_INVAL
 
 
@@ -157,5 +157,5 @@ def test_batch_solve_without_gpu_fails_loudly(hq):
     dp = ctypes.POINTER(ctypes.c_double)
     st = lib.hq_batch_solve(1, 3, 2, lam.ctypes.data_as(dp), mu.ctypes.data_as(dp),
                             pref.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), 1e-13, 100, ctypes.c_void_p(16),
-                            None, None, None, None)
+                            None, None, None, None, None, None, None)
     assert st == hq.HQ_E_CUDA

@@ -34,8 +34,14 @@ def test_batch_mixed_n9(hq):
     for k, rho in enumerate([0.1, 0.3, 0.5, 0.7, 0.9, 0.95]):
         for L in (None, 4):
             insts.append(hqinst.generate(9, 30, seed=100 + k, rho=rho, L=L, clustered=bool(k % 2)))
-    pi, it, res, st = hq.hq_batch_solve(*stack(insts), tol=TOL)
+    meas = {}
+    pi, it, res, st = hq.hq_batch_solve(*stack(insts), tol=TOL, measures=meas)
     check_against_oracle(insts, pi, it, res, st)
+    for b, inst in enumerate(insts):   # measures vs the oracle's, on the GPU pi
+        w, d, loss = oracle.measures(inst, pi[b].cpu().numpy())
+        assert np.abs(meas["workload"][b].cpu().numpy() - w).max() <= 1e-12
+        assert np.abs(meas["dispatch"][b].cpu().numpy() - d).max() <= 1e-12
+        assert abs(meas["loss"][b] - loss) <= 1e-12
 
 
 def test_batch_rho_sweep_n11(hq):

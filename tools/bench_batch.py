@@ -32,12 +32,12 @@ for (N, J, B) in [(9, 71, 1332), (6, 99, 1332), (11, 71, 1332), (12, 71, 592)]:
     mu = np.stack([i.mu for i in insts])
     pref = np.stack([i.pref for i in insts]).astype(np.int32)
     pi = torch.empty((B, 1 << N), dtype=torch.float64, device="cuda")
-    hq.hq_batch_solve(lam, mu, pref, tol=1e-13, pi=pi)   # warm-up
+    hq.hq_batch_solve(lam, mu, pref, tol=1e-13, pi=pi, measures={})   # warm-up
     ts = []
     for _ in range(3):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        _, it, res, st = hq.hq_batch_solve(lam, mu, pref, tol=1e-13, pi=pi)
+        _, it, res, st = hq.hq_batch_solve(lam, mu, pref, tol=1e-13, pi=pi, measures={})
         torch.cuda.synchronize()
         ts.append(time.perf_counter() - t0)
     t = min(ts)
