@@ -375,7 +375,6 @@ struct hq_problem {
     int nW = 0;                    // path 3: log2(warps per CTA)
     int nslots = 0;                // path 3: CTA ring slots
     uint32_t maxblk_all = 0;       // path 3: largest program block of a CTA tile (records)
-    unsigned *d_done = nullptr;    // path 3: CTA completion counter of the fused scalar step
     unsigned long long *d_wtime = nullptr;   // path 3: per-warp busy cycles (-DHQ_WARP_TIMING builds)
     int prog_nwv = 0;              // path 3: warp bits varying inside a rate program (nW: CTA programs)
     float tune_ms[2] = {0.f, 0.f}; // path 3: timed sweeps with CTA / warp programs (0: not tuned)
@@ -416,8 +415,6 @@ struct hq_problem {
         dfree(d_order);
         dfree(d_range);
         d_range = nullptr;
-        dfree(d_done);
-        d_done = nullptr;
         dfree(d_wtime);
         d_wtime = nullptr;
         dfree(d_off16);
@@ -775,10 +772,6 @@ static hq_status v2_prepare(hq_problem *h, cudaStream_t s) {
         dfree(h->d_range);
         h->d_range = nullptr;
         HQ_CUDA(dmalloc((void **)&h->d_range, 4 * (G + 1)));
-        if (!h->d_done) {
-            HQ_CUDA(dmalloc((void **)&h->d_done, sizeof(unsigned)));
-            HQ_CUDA(cudaMemset(h->d_done, 0, sizeof(unsigned)));
-        }
         HQ_CUDA(cudaMemcpy(h->d_range, range.data(), 4 * (G + 1), cudaMemcpyHostToDevice));
     }
     dfree(tmp);
@@ -928,8 +921,6 @@ static hq_status v3_programs(hq_problem *h, cudaStream_t s, int nwv, const std::
     std::vector<uint32_t> off16(ntiles << nW);
     std::vector<double> cost(ntiles);
     double tot = 0.0;
-    const int cost_model = getenv("HQ_COST") ? atoi(getenv("HQ_COST")) : 0;   // development switch
-    const double cost_base = getenv("HQ_COST_BASE") ? atof(getenv("HQ_COST_BASE")) : 263.0;
     ps.maxblk = 0;
     for (uint64_t i = 0; i < ntiles; i++) {
         uint32_t b = 0, bmax = 0;
@@ -946,9 +937,7 @@ static hq_status v3_programs(hq_problem *h, cudaStream_t s, int nwv, const std::
         // the evaluation of the program records (every warp evaluates a CTA program).  Chosen
         // by same-box A/B timing; models fitted to per-warp busy cycles balanced worse.
         cost[i] = 256.0 + (double)b * (per_warp ? 1.0 : (double)W / 4.0);
-        if (cost_model == 1) cost[i] = cost_base + (double)bmax;   // slowest warp's program
-        if (cost_model == 3) cost[i] = cost_base + (double)b;      // per-tile base in records
-        if (cost_model == 2) cost[i] = cost_base + 0.5 * (double)bmax + 0.5 * (double)b / W;
+
         tot += cost[i];
     }
     HQ_CUDA(cudaMemcpyAsync(ps.off16, off16.data(), 4 * off16.size(), cudaMemcpyHostToDevice, s));
@@ -1084,10 +1073,6 @@ static hq_status v3_prepare(hq_problem *h, cudaStream_t s) {
     const int g = h->nsm * 8;
     if (!h->full_lists) HQ_CUDA(hq2_launch::lambda_states(pa, h->d_lamarr, g, s));
     HQ_CUDA(hq2_launch::omkap(pa, h->d_lamarr, h->d_omkap, g, s));
-    if (!h->d_done) {
-        HQ_CUDA(dmalloc((void **)&h->d_done, sizeof(unsigned)));
-        HQ_CUDA(cudaMemsetAsync(h->d_done, 0, sizeof(unsigned), s));
-    }
     // program granularity: warp programs (warp bits folded; fewer pairs per thread; the
     // default) or CTA programs (warps share one program).  HQ_PROG=cta forces CTA programs;
     // HQ_PROG=auto builds both and keeps the faster sweep (timing-dependent, so results may
@@ -1183,8 +1168,6 @@ static cudaError_t tiled_sweep(hq_problem *h, const S2Args &sa, int mode, cudaSt
     a.maxblk16 = sa.maxrec;
     a.nslots = h->nslots;
     a.range = h->d_range;
-    a.blk = h->d_blk;
-    a.done = h->d_done;
     a.full_lists = sa.full_lists;
     a.warp_programs = (h->prog_nwv == 0) ? 1 : 0;
     a.all_staged = h->maxblk_all <= h->maxrec ? 1 : 0;
@@ -1287,7 +1270,7 @@ static hq_status solve_v2(hq_problem *h, double tol, int max_iter, double *pi, c
     // (S3Args::fold): the scalar block and the CTA partials are double-buffered; a pending
     // step is resolved by k_scalars2 before the host reads the block or a residual runs.
     // (only where the per-CTA partial reduction is short: <= 48 loads per thread)
-    const bool fold = h->path == 3 && !hq3_launch::fused_scalars() && !getenv("HQ_NOFOLD") &&
+    const bool fold = h->path == 3 && !getenv("HQ_NOFOLD") &&
                       (size_t)h->sgrid * (N + 1) * NV2 <= (size_t)48 * (32u << h->nW);
     double *blkp[2] = {h->d_blk, h->d_blk + V2S_TOTAL};
     double *part[2] = {h->d_partial, h->d_partial + (size_t)std::max(h->grid, h->sgrid) * HQ_NL * HQ_NV};
@@ -1339,7 +1322,7 @@ static hq_status solve_v2(hq_problem *h, double tol, int max_iter, double *pi, c
             pc_prev = c;
             pa_prev = active;
             pw ^= 1;
-        } else if (h->path != 3 || !hq3_launch::fused_scalars()) {   // path 3 fused: scalar step in the sweep's last CTA
+        } else {
             HQ_CUDA(hq2_launch::scalars(N, sa.full_lists, h->Lam, 1, c, active, h->sgrid, h->d_partial, h->d_blk, s,
                                         h->path == 3 ? 1 : 0));
             o.launches++;

@@ -45,11 +45,6 @@
 namespace hq3 {
 
 constexpr int R = V3_R;
-#ifdef HQ_FUSED_SCALARS
-constexpr bool kFusedScalars = true;    // A/B variant: scalar step in the sweep kernel's last CTA
-#else
-constexpr bool kFusedScalars = false;   // scalar step as its own launch (k_scalars2): measured faster
-#endif
 
 __device__ __forceinline__ double warp_sum(double s) {
 #pragma unroll
@@ -306,10 +301,6 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
 #else
         if (staged) bulk_g2s(sptr(b + TS), a.prog + o, nrec * 16u, bar);
 #endif
-#ifdef HQ_OMKAP_PREFETCH
-        // the tile's scatter weights (read once, in the epilogue) into L2 a tile ahead
-        if (MODE < 2) prefetch_l2(a.omkap + ((size_t)t << T), TS * 16u);
-#endif
     };
     if (tid == 0) {
         mbar_init(sptr(&tbar[0]), 1);
@@ -424,20 +415,6 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
         const uint32_t t = __ldg(a.order + tidx);
         const uint32_t jt = t << T;
         const int buf = k & 1;
-#ifdef HQ_HLOOP3
-        // tile-unit neighbour slices: three rotating buffers, each refilled right after it is
-        // consumed (two units of loads in flight ahead of the one accumulated, no copies)
-        const double *qb = a.Q + (jt | jw);
-        auto hload = [&](int h, double2 (&B)[4]) {
-            const size_t off = (size_t)1 << (T + h);
-            const double *src = ((t >> h) & 1u) ? qb - off : qb + off;
-#pragma unroll
-            for (int kk = 0; kk < 4; kk++) B[kk] = ldg2(src + (kk << 6), pol_el);
-        };
-        double2 B0[4], B1[4], B2[4];
-        if (nH > 0) hload(0, B0);
-        if (nH > 1) hload(1, B1);
-#else
         // tile-unit neighbour slices: two units of loads in flight ahead of the one accumulated
         auto hsrc = [&](int h) -> const double * { return a.Q + ((jt ^ (1u << (T + h))) | jw); };
         double2 pa[4], pb2[4];
@@ -449,7 +426,6 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
 #pragma unroll
             for (int kk = 0; kk < 4; kk++) pb2[kk] = ldg2(hsrc(1) + (kk << 6), pol_el);
         }
-#endif
         mbar_wait(sptr(&tbar[buf]), (unsigned)((k >> 1) & 1));
         __syncthreads();   // every warp is done with tile k-1: its buffer may be refilled
         if (tid == 0 && k + 1 < nt) {
@@ -519,9 +495,6 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
                 else D[r] = fma(nuu, q[r], D[r]);
             }
         }
-#ifdef HQ_HLOOP3
-        if (nH > 2) hload(2, B2);   // qo is dead: room for the third buffer
-#endif
         // ---- lane units 2..6 (lane bits 0..4): busy per lane
 #pragma unroll
         for (int b = 0; b < 5; b++) {
@@ -564,40 +537,6 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
                 for (int r = 0; r < R; r++) D[r] = fma(nuu, q[r], D[r]);
             }
         }
-#ifdef HQ_HLOOP3
-        // ---- tile units (H): neighbour tile slices straight from global memory (L2)
-        auto unit_H = [&](int h, const double2 (&B)[4]) {
-            const int u = NVU + h;
-            double qh[R];
-#pragma unroll
-            for (int kk = 0; kk < 4; kk++) {
-                qh[2 * kk] = B[kk].x;
-                qh[2 * kk + 1] = B[kk].y;
-            }
-            if ((t >> h) & 1u) {
-                const uint4 hu = P.hdr(u);
-                const double Wt = unit_rates(P, hu, sh, hdr_w0(hu), qh, A);
-#pragma unroll
-                for (int r = 0; r < R; r++) A[r] = fma(Wt, qh[r], A[r]);
-            } else {
-                const double nuu = a.nu[u];
-#pragma unroll
-                for (int r = 0; r < R; r++) D[r] = fma(nuu, qh[r], D[r]);
-            }
-        };
-        for (int h = 0; h < nH; h += 3) {
-            unit_H(h, B0);
-            if (h + 3 < nH) hload(h + 3, B0);
-            if (h + 1 < nH) {
-                unit_H(h + 1, B1);
-                if (h + 4 < nH) hload(h + 4, B1);
-            }
-            if (h + 2 < nH) {
-                unit_H(h + 2, B2);
-                if (h + 5 < nH) hload(h + 5, B2);
-            }
-        }
-#else
         // ---- tile units (H): neighbour tile slices straight from global memory (L2), two
         //      units of loads in flight; unrolled by two so the buffers alternate in place
         auto unit_H = [&](int h, double2 (&buf)[4]) {
@@ -627,7 +566,6 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
             unit_H(h, pa);
             if (h + 1 < nH) unit_H(h + 1, pb2);
         }
-#endif
         // ---- lambda_m: Lambda minus the atoms whose whole (truncated) list is busy
         double lam[R];
         if (FULL) {
@@ -763,59 +701,6 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
             for (int v = 0; v < NV2; v++) a.partial[((size_t)lane * HQ_NV + v) * G + blockIdx.x] = o[v];
         }
     }
-    if (MODE == 2 || !kFusedScalars) return;
-    // ---- the last CTA to finish reduces the partials (fixed CTA order) and performs the
-    //      scalar step of the half-sweep (hq_scalars.cuh): no separate launch
-    __shared__ int s_last;
-    __shared__ double S[HQ_NL][NV2];
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) s_last = atomicAdd(a.done, 1u) == (unsigned)(G - 1);
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    // (layer, value) pair i = tid % 160 summed over CTA chunk tid / 160 (fixed order), then
-    // the chunks in order: all loads of a thread are independent and in flight together
-    {
-        constexpr int NP = HQ_NL * NV2;
-        const int nchunk = (int)blockDim.x / NP;   // 3 at 512 threads, 1 at >= 160 threads
-        double *cs = tileq;                        // [nchunk][NP]
-        if (nchunk >= 1 && tid < nchunk * NP) {
-            const int i = tid % NP, ch = tid / NP;
-            const int n = i / NV2, v = i - n * NV2;
-            const double *src = a.partial + ((size_t)n * HQ_NV + v) * G;
-            const int b0 = (G * ch) / nchunk, b1 = (G * (ch + 1)) / nchunk;
-            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-            int b = b0;
-            for (; b + 3 < b1; b += 4) {
-                s0 += __ldcg(src + b);
-                s1 += __ldcg(src + b + 1);
-                s2 += __ldcg(src + b + 2);
-                s3 += __ldcg(src + b + 3);
-            }
-            for (; b < b1; b++) s0 += __ldcg(src + b);
-            cs[ch * NP + i] = (s0 + s1) + (s2 + s3);
-        }
-        __syncthreads();
-        for (int i = tid; i < NP; i += blockDim.x) {
-            double s = 0.0;
-            if (nchunk >= 1) {
-                for (int ch = 0; ch < nchunk; ch++) s += cs[ch * NP + i];
-            } else {   // fewer than 160 threads: one pair at a time per thread
-                const int n = i / NV2, v = i - n * NV2;
-                const double *src = a.partial + ((size_t)n * HQ_NV + v) * G;
-                for (int b = 0; b < G; b++) s += __ldcg(src + b);
-            }
-            S[i / NV2][i % NV2] = s;
-        }
-    }
-    // the scalar step runs on a shared-memory copy of the block (one thread, serial)
-    double *sblk = tileq + 3 * HQ_NL * NV2;
-    for (int i = tid; i < V2S_TOTAL; i += blockDim.x) sblk[i] = __ldcg(a.blk + i);
-    __syncthreads();
-    scalars_update(a.N, a.full_lists, a.Lam, 1, a.c, a.active, S, sblk);
-    if (tid == 0) *a.done = 0u;
-    for (int i = tid; i < V2S_TOTAL; i += blockDim.x) a.blk[i] = sblk[i];
 }
 
 // ---------------------------------------------------------------------------
@@ -1106,7 +991,6 @@ __global__ void k_prog_write3(P3Args a, const uint32_t *__restrict__ order, cons
 // ---------------------------------------------------------------------------
 namespace hq3_launch {
 
-bool fused_scalars() { return hq3::kFusedScalars; }
 
 int choose_nw(int N) {
     int nw = N - 9 - 8;   // keep >= 256 tiles while the CTA is narrower than 16 warps

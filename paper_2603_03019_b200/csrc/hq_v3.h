@@ -56,8 +56,6 @@ struct S3Args {
     const double2 *omkap;    // scatter weights of class c
     const double *coef;      // v2 scalar block (V2S_* offsets)
     double *partial;         // MODE 2: [grid][HQ_NL][HQ_NV]; MODE 0/1: [HQ_NL][HQ_NV][grid]
-    double *blk;             // the scalar block, updated by the last CTA (MODE 0/1)
-    unsigned *done;          // CTA completion counter (self-resetting)
     int full_lists;
     int warp_programs;       // 1: one rate program per warp tile (tables over lane bits only)
     int all_staged;          // 1: every tile's program block fits the staged capacity (maxblk16)
@@ -95,5 +93,4 @@ int choose_slots(int nW, uint32_t maxblk16);
 uint32_t choose_cap(int nW, uint32_t maxblk16);
 int choose_nw(int N);
 int ctas_per_sm(int nW);   // CTAs per SM the sweep grid is sized for
-bool fused_scalars();
 }  // namespace hq3_launch
