@@ -155,6 +155,21 @@ def cpu_sample_sweeps(N):
     return max(1, min(64, 16 << max(0, 24 - N)))
 
 
+def reduce_over_ranks(t, work, device):
+    """Replicas only: the job takes as long as the slowest rank and does the
+    work of all ranks -> (max over ranks of t, sum over ranks of work).  Works for any
+    torch.distributed backend (nccl with a CUDA device, gloo with the CPU)."""
+    import torch
+    import torch.distributed as dist
+
+    x = torch.tensor([t, work], dtype=torch.float64, device=device)
+    mx = x.clone()
+    dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+    sm = x.clone()
+    dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+    return float(mx[0]), float(sm[1])
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return 0
@@ -246,15 +261,7 @@ def run_ours(args, rank, world, local_rank):
         dist.barrier()
     ck = clocks.stop()
     ms = e0.elapsed_time(e1)
-    if dist:
-        t = torch.tensor([ms, updates], dtype=torch.float64, device=dev)
-        mx = t.clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        sm = t.clone()
-        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
-        ms_max, updates_tot = float(mx[0]), float(sm[1])
-    else:
-        ms_max, updates_tot = ms, updates
+    ms_max, updates_tot = reduce_over_ranks(ms, updates, dev) if dist else (ms, updates)
 
     # ---- e2e: through the C-ABI with host buffers, h2d + d2h inside the timed region
     e2e = None
@@ -283,12 +290,7 @@ def run_ours(args, rank, world, local_rank):
             s2.close()
         t_e2e = time.perf_counter() - t0
         if dist:
-            t = torch.tensor([t_e2e, e2e_updates], dtype=torch.float64, device=dev)
-            mx = t.clone()
-            dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-            sm = t.clone()
-            dist.all_reduce(sm, op=dist.ReduceOp.SUM)
-            t_e2e, e2e_updates = float(mx[0]), float(sm[1])
+            t_e2e, e2e_updates = reduce_over_ranks(t_e2e, e2e_updates, dev)
         h2d = inst.lam.nbytes + inst.mu.nbytes + inst.pref.nbytes
         d2h = (8 << inst.N) + 8 * inst.N + 8 * inst.J * inst.N + 8 + 8
         e2e = {"value": e2e_updates / t_e2e, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
