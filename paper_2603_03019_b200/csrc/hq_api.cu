@@ -352,6 +352,8 @@ struct hq_problem {
     bool solved = false;
     // waiting room (hq_set_buffer): 0 loss system, C > 0 finite buffer, -1 unlimited
     int bufC = 0;
+    cudaStream_t side = nullptr;   // path 3 precompute: scatter weights beside the rate programs
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     double q_r = 0.0;        // Lambda / sum nu
     double q_first = 0.0;    // P~{1} of the last solve
     double q_mass = 0.0;     // sum_c P~{c}
@@ -423,6 +425,9 @@ struct hq_problem {
         dfree(d_omkap);
         dfree(d_lamarr);
         dfree(d_blk);
+        if (side) cudaStreamDestroy(side);
+        if (ev_fork) cudaEventDestroy(ev_fork);
+        if (ev_join) cudaEventDestroy(ev_join);
         pinned_free(h_blk, sizeof(double) * V2S_TOTAL);
         d_order = d_off16 = d_size16 = nullptr;
         d_prog = nullptr;
@@ -1071,8 +1076,18 @@ static hq_status v3_prepare(hq_problem *h, cudaStream_t s) {
     cudaEvent_t e0 = h->event(2), e1 = h->event(3);
     HQ_CUDA(cudaEventRecord(e0, s));
     const int g = h->nsm * 8;
-    if (!h->full_lists) HQ_CUDA(hq2_launch::lambda_states(pa, h->d_lamarr, g, s));
-    HQ_CUDA(hq2_launch::omkap(pa, h->d_lamarr, h->d_omkap, g, s));
+    // the scatter weights (and lambda_m) are independent of the rate programs: a side stream
+    // builds them while the programs are built and partitioned on s
+    if (!h->side) {
+        HQ_CUDA(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
+        HQ_CUDA(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+        HQ_CUDA(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
+    }
+    HQ_CUDA(cudaEventRecord(h->ev_fork, s));
+    HQ_CUDA(cudaStreamWaitEvent(h->side, h->ev_fork, 0));
+    if (!h->full_lists) HQ_CUDA(hq2_launch::lambda_states(pa, h->d_lamarr, g, h->side));
+    HQ_CUDA(hq2_launch::omkap(pa, h->d_lamarr, h->d_omkap, g, h->side));
+    HQ_CUDA(cudaEventRecord(h->ev_join, h->side));
     // program granularity: warp programs (warp bits folded; fewer pairs per thread; the
     // default) or CTA programs (warps share one program).  HQ_PROG=cta forces CTA programs;
     // HQ_PROG=auto builds both and keeps the faster sweep (timing-dependent, so results may
@@ -1088,6 +1103,7 @@ static hq_status v3_prepare(hq_problem *h, cudaStream_t s) {
         st = v3_programs(h, s, h->nW, order, a);
         if (st != HQ_OK) return st;
     } else {
+        HQ_CUDA(cudaStreamWaitEvent(s, h->ev_join, 0));   // the timed sweeps read omega/kappa
         float tc = INFINITY, tw = INFINITY;
         st = v3_programs(h, s, h->nW, order, a);
         if (st == HQ_OK) {
@@ -1139,6 +1155,7 @@ static hq_status v3_prepare(hq_problem *h, cudaStream_t s) {
         h->err = "tile working set exceeds the shared-memory budget";
         return HQ_E_NUMERIC;
     }
+    HQ_CUDA(cudaStreamWaitEvent(s, h->ev_join, 0));
     HQ_CUDA(cudaEventRecord(e1, s));
     HQ_CUDA(cudaEventSynchronize(e1));
     float ms = 0.f;
