@@ -858,12 +858,15 @@ static hq_status v3_programs(hq_problem *h, cudaStream_t s, int nwv, const std::
     }
     uint32_t *d_pord = nullptr, *d_size = nullptr, *d_offp = nullptr, *d_max = nullptr;
     void *tmp = nullptr;
+    void *cache = nullptr;   // pair cache of the count pass (see below)
     auto cleanup = [&]() {
         dfree(d_pord);
         dfree(d_size);
         dfree(d_offp);
         dfree(d_max);
         dfree(tmp);
+        dfree(cache);
+        cache = nullptr;
     };
     if (dmalloc((void **)&d_pord, 4 * nprog) != cudaSuccess || dmalloc((void **)&d_size, 4 * nprog) != cudaSuccess ||
         dmalloc((void **)&d_offp, 4 * nprog) != cudaSuccess) {
@@ -886,6 +889,25 @@ static hq_status v3_programs(hq_problem *h, cudaStream_t s, int nwv, const std::
     p3.lam_thr = h->d_lthr;
     p3.lam_end = h->d_lend;
     const int g = h->nsm * 8;
+    // pair cache for the write pass: up to 256 MB, at most 512 pairs per program
+    {
+        const uint64_t budget = 256ull << 20;
+        const int64_t per = (int64_t)(budget / nprog) - 32 * 8;
+        const int ccap = (int)std::min<int64_t>(512, per > 0 ? per / 14 : 0);
+        if (ccap >= 32 && dmalloc(&cache, nprog * ((size_t)ccap * 14 + 32 * 8 + 4)) == cudaSuccess) {
+            char *c = static_cast<char *>(cache);
+            p3.ccap = ccap;
+            p3.cval = reinterpret_cast<double *>(c);
+            c += nprog * (size_t)ccap * 8;
+            p3.cW0 = reinterpret_cast<double *>(c);
+            c += nprog * 32 * 8;
+            p3.ckey = reinterpret_cast<uint32_t *>(c);
+            c += nprog * (size_t)ccap * 4;
+            p3.cn = reinterpret_cast<int *>(c);
+            c += nprog * 4;
+            p3.crm = reinterpret_cast<uint16_t *>(c);
+        }
+    }
     HQ_CUDA(cudaMemsetAsync(h->d_err, 0, sizeof(int), s));
     HQ_CUDA(hq3_launch::prog_count(p3, d_pord, d_size, h->d_err, g, s));
     size_t tb = 0;

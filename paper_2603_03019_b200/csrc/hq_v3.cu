@@ -895,9 +895,23 @@ __global__ void k_prog_count3(P3Args a, const uint32_t *__restrict__ order, uint
         if (nrec < 0 || nrec >= 65536) {
             atomicExch(err, 2);
             size16[i] = V3_HDR16;
+            if (a.ccap > 0) a.cn[i] = -1;
             continue;
         }
         size16[i] = V3_HDR16 + (uint32_t)nrec;
+        if (a.ccap > 0) {
+            const bool fits = P.n <= a.ccap;
+            a.cn[i] = fits ? P.n : -1;
+            if (fits) {
+                const uint64_t o = i * (uint64_t)a.ccap;
+                for (int k = 0; k < P.n; k++) {
+                    a.ckey[o + k] = P.key[k];
+                    a.cval[o + k] = P.val[k];
+                    a.crm[o + k] = P.rm[k];
+                }
+                for (int u = 0; u < 32; u++) a.cW0[i * 32 + u] = u <= HQ_MAXN ? W0[u] : 0.0;
+            }
+        }
     }
 }
 
@@ -920,7 +934,19 @@ __global__ void k_prog_write3(P3Args a, const uint32_t *__restrict__ order, cons
          i += (uint64_t)gridDim.x * blockDim.x) {
         uint4 *out = prog + off16[i];
         const uint32_t t = order[i];
-        if (tile_program(a, t, W0, P) < 0) continue;
+        const int cached = a.ccap > 0 ? a.cn[i] : -1;
+        if (cached >= 0) {   // the count pass's sorted pairs
+            const uint64_t o = i * (uint64_t)a.ccap;
+            P.n = cached;
+            for (int k = 0; k < cached; k++) {
+                P.key[k] = a.ckey[o + k];
+                P.val[k] = a.cval[o + k];
+                P.rm[k] = a.crm[o + k];
+            }
+            for (int u = 0; u <= HQ_MAXN; u++) W0[u] = a.cW0[i * 32 + u];
+        } else if (tile_program(a, t, W0, P) < 0) {
+            continue;
+        }
         uint32_t info[32], infm[32];
         for (int q = 0; q < 32; q++) info[q] = infm[q] = 0u;
         uint4 *data = out + V3_HDR16;
@@ -983,6 +1009,7 @@ __global__ void k_prog_write3(P3Args a, const uint32_t *__restrict__ order, cons
             if (info[q]) has |= 1u << q;
         out[32] = make_uint4((uint32_t)__double_as_longlong(muF),
                              (uint32_t)((unsigned long long)__double_as_longlong(muF) >> 32), has, 0u);
+        if (cached >= 0) P.n = 0;   // the hash index was not used: nothing to reset
     }
 }
 

@@ -81,6 +81,14 @@ struct P3Args {   // program precompute (one program per warp tile or per CTA ti
     const int2 *node;        // .x = unit | depth << 8, .y = skip
     const double *lam_thr;
     const double *lam_end;
+    // pair cache (optional, ccap > 0): the count pass stores each program's sorted pairs
+    // (<= ccap of them) and W0 so that the write pass does not walk the trie again
+    int ccap;
+    uint32_t *ckey;          // [ntiles][ccap]
+    double *cval;            // [ntiles][ccap]
+    uint16_t *crm;           // [ntiles][ccap]
+    double *cW0;             // [ntiles][32]
+    int *cn;                 // [ntiles]: number of pairs, -1 if not cached
 };
 
 namespace hq3_launch {
