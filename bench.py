@@ -155,6 +155,15 @@ def cpu_sample_sweeps(N):
     return max(1, min(64, 16 << max(0, 24 - N)))
 
 
+def arm_config(inst, args, world):
+    """The config block both arms print (same workload, tolerance and L2 statement)."""
+    return dict(workload_desc(inst, args.config), tol=args.tol,
+                l2="inputs larger than L2: per half-sweep the kernel streams %.0f MB (both classes of p, "
+                   "omega/kappa, rate programs) vs 126 MB L2; no explicit flush"
+                   % ((8 + 8 + 16) * (1 << inst.N) / 2 / 2 ** 20),
+                parallelism="replicas" if world > 1 else "single GPU")
+
+
 def reduce_over_ranks(t, work, device):
     """Replicas only: the job takes as long as the slowest rank and does the
     work of all ranks -> (max over ranks of t, sum over ranks of work).  Works for any
@@ -191,7 +200,7 @@ def run_reference(args, rank, world):
     line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * tt / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": workload_desc(inst, args.config),
+            "config": arm_config(inst, args, world),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -323,11 +332,7 @@ def run_ours(args, rank, world, local_rank):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded EMS-shaped instance, hqinst)",
-            "config": dict(workload_desc(inst, args.config), tol=args.tol,
-                           l2="inputs larger than L2: per half-sweep the kernel streams %.0f MB (both classes of p, "
-                              "omega/kappa, rate programs) vs 126 MB L2; no explicit flush"
-                              % ((8 + 8 + 16) * (1 << inst.N) / 2 / 2 ** 20),
-                           parallelism="replicas" if world > 1 else "single GPU"),
+            "config": arm_config(inst, args, world),
             "time_to_tol_ms": statistics.median(solve_ms), "sweeps": statistics.median(iters),
             "residual": max(res), "roofline": roofline, "gpu_launches": int(launches),
             "e2e": e2e}
