@@ -19,17 +19,25 @@
 // sweep launch, layers 0..N: a group of tpi = 2^lg threads per (layer, value) (lg 0..5),
 // each thread with four interleaved accumulators (loads in flight), combined in a fixed
 // order (deterministic).  No barrier.
-__device__ __forceinline__ void reduce_partials_t(const double *partial, int G, int N, double (*S)[NV2], int lg) {
-    const int items = (N + 1) * NV2;
+// only: 0 = every layer 0..N, else a mask of the layers to reduce (the others are left as they are)
+__device__ __forceinline__ void reduce_partials_t(const double *partial, int G, int N, double (*S)[NV2], int lg,
+                                                  uint32_t only = 0u) {
+    int lay[HQ_NL];   // the reduced layers, ascending
+    int nl = 0;
+    for (int L = 0; L <= N; L++)
+        if (!only || ((only >> L) & 1u)) lay[nl++] = L;
+    const int items = nl * NV2;
     const int tpi = 1 << lg, q = threadIdx.x & (tpi - 1);
     // items rounded up to whole warps: every warp visits its items together, so the
     // shuffles below are warp-uniform (blockDim.x is a multiple of 32)
     const int per_warp = 32 >> lg;
     const int nit = (items + per_warp - 1) / per_warp * per_warp;
     for (int it = threadIdx.x >> lg; it < nit; it += blockDim.x >> lg) {
-        const int L = it / NV2, v = it - L * NV2;
+        const int li = it / NV2, v = it - li * NV2;
+        const bool ok = li < nl;
+        const int L = ok ? lay[li] : 0;
         double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-        if (L <= N) {
+        if (ok) {
             const double *src = partial + ((size_t)L * HQ_NV + v) * G;
             int b = q;
             for (; b + 3 * tpi < G; b += 4 * tpi) {
@@ -42,7 +50,7 @@ __device__ __forceinline__ void reduce_partials_t(const double *partial, int G, 
         }
         double s = (s0 + s1) + (s2 + s3);
         for (int o = 1; o < tpi; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (q == 0 && L <= N) S[L][v] = s;
+        if (q == 0 && ok) S[L][v] = s;
     }
 }
 

@@ -319,7 +319,7 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
         double(*s_S)[NV2] = reinterpret_cast<double(*)[NV2]>(tileq + BUFD);
         double *s_blk = tileq + BUFD + HQ_NL * NV2;
         for (int i = tid; i < V2S_TOTAL; i += blockDim.x) s_blk[i] = a.coef[i];
-        reduce_partials_t(a.prev_partial, gridDim.x, a.N, s_S, 2);
+        reduce_partials_t(a.prev_partial, gridDim.x, a.N, s_S, 2, a.prev_active);   // the step reads these only
         __syncthreads();
         scalars_update(a.N, a.full_lists, a.Lam, 1, a.prev_c, a.prev_active, s_S, s_blk);
         if (blockIdx.x == 0)
