@@ -82,3 +82,13 @@ def test_batch_not_converged_status(hq):
     insts = [hqinst.generate(9, 30, seed=1, rho=0.9)]
     pi, it, res, st = hq.hq_batch_solve(*stack(insts), tol=TOL, max_iter=3)
     assert st[0] == hq.HQ_NOT_CONVERGED and it[0] == 3 and res[0] > TOL
+
+
+def test_batch_more_instances_than_ctas(hq):
+    """B larger than the resident grid: every CTA loops over several instances."""
+    insts = [hqinst.generate(4, 5, seed=s, rho=0.2 + 0.7 * (s % 10) / 10) for s in range(3000)]
+    pi, it, res, st = hq.hq_batch_solve(*stack(insts), tol=TOL)
+    assert (st == 0).all() and (res <= TOL).all()
+    for b in range(0, 3000, 211):
+        lu = dense.stationary(insts[b].lam, insts[b].mu, insts[b].pref)
+        assert np.abs(pi[b].cpu().numpy() - lu).max() <= 1e-13

@@ -98,3 +98,15 @@ def test_buffer_cfg3_against_fixture(hq, C):
     assert abs(g["dispatch"].sum() - 1.0) <= 1e-12
     np.testing.assert_allclose(inst.mu * g["workload"], Lam * (1.0 - g["loss"]) * g["dispatch"].sum(axis=0),
                                rtol=1e-10, atol=1e-12)
+
+
+@pytest.mark.parametrize("N", [3, 5, 8])
+def test_buffer_small_paths(hq, N):
+    """The two-pass path (N < 8) and the warp-tiled path (N = 8) take the same waiting room."""
+    inst = hqinst.generate(N, 6, seed=N, rho=0.8)
+    for C in (2, U):
+        g = gpu_solve_buffer(hq, inst, C)
+        pi_d, tail_d = buffer.stationary_buffer(inst.lam, inst.mu, inst.pref, 300 if C == U else C)
+        assert np.abs(g["pi"] - pi_d).max() <= 1e-12
+        n = len(g["tail"])
+        np.testing.assert_allclose(g["tail"], tail_d[:n], rtol=0, atol=1e-12)
