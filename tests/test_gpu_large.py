@@ -152,3 +152,12 @@ def test_ordered_hunt_n31_closed_form(hq):
     assert abs(g["loss"] - B[N]) <= 1e-12
     w = np.array([math.exp(n * math.log(a) - math.lgamma(n + 1)) for n in range(N + 1)])
     np.testing.assert_allclose(layer_masses(g["pi"], N), w / w.sum(), rtol=0, atol=1e-12)
+
+
+def test_cfg3_bitwise_deterministic(hq):
+    """The N >= 21 path (folded scalar step, double-buffered partials, fixed-order sums) gives
+    bitwise identical results on two handles."""
+    inst = hqinst.config_instance(3)
+    a = solve(hq, inst)
+    b = solve(hq, inst)
+    assert torch.equal(a["pi"], b["pi"]) and a["iters"] == b["iters"] and a["residual"] == b["residual"]
