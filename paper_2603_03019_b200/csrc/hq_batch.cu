@@ -39,6 +39,7 @@ struct BArgs {
     double tol;
     int max_iter;
     int check;               // residual every `check` sweeps
+    int maxc;                // largest layer, C(N, N/2): size of the x / y scratch
     double *pi;              // [B][2^N] natural index
     int *iters;              // [B]
     double *res;             // [B]
@@ -101,8 +102,8 @@ __global__ void __launch_bounds__(kThreads) k_batch_solve(BArgs a) {
     double *p = reinterpret_cast<double *>(smem);   // p_n(B_m), natural index
     double *lamm = p + S;                            // lambda_m
     double *mum = lamm + S;                          // mu_m
-    double *xs = mum + S;                            // per-layer scratch x_m, y_m (layer order)
-    double *ys = xs + S;
+    double *xs = mum + S;                            // per-layer scratch x_m, y_m (layer-local order)
+    double *ys = xs + a.maxc;
     __shared__ double2 scr[kThreads / 32];
     __shared__ double s_lam[kMaxN + 2], s_mu[kMaxN + 2], s_nu[kMaxN], s_pn[kMaxN + 2];
 
@@ -156,8 +157,8 @@ __global__ void __launch_bounds__(kThreads) k_batch_solve(BArgs a) {
                     }
                     const double den = lamm[m] + mum[m];
                     const double x = A / (lprev * den), y = beta * D / den;
-                    xs[k] = x;
-                    ys[k] = y;
+                    xs[k - o0] = x;
+                    ys[k - o0] = y;
                     sx += x;
                     sy += y;
                 }
@@ -167,7 +168,7 @@ __global__ void __launch_bounds__(kThreads) k_batch_solve(BArgs a) {
                 double sl = 0.0, sm = 0.0;
                 for (int k = o0 + tid; k < o1; k += blockDim.x) {
                     const uint32_t m = a.order[k];
-                    const double v = mstar * xs[k] + ys[k];
+                    const double v = mstar * xs[k - o0] + ys[k - o0];
                     p[m] = v;
                     sl += v * lamm[m];
                     sm += v * mum[m];
@@ -224,7 +225,7 @@ __global__ void __launch_bounds__(kThreads) k_batch_solve(BArgs a) {
             // g(T) = sum_{m superset of T} pi(m) by an in-place zeta transform (fixed order), then
             //   rho_i = g({i}),  loss = sum_j f_j g(list_j),
             //   rho_ij = f_j (g(units before i in zeta_j) - g(units through i)) / (1 - loss)
-            double *g = xs;
+            double *g = mum;   // mu_m is rebuilt for the next instance
             for (uint32_t m = tid; m < S; m += blockDim.x) g[m] = s_pn[__popc(m)] * p[m];
             for (int bit = 0; bit < N; bit++) {
                 __syncthreads();
@@ -400,12 +401,14 @@ extern "C" hq_status hq_batch_solve(int B, int N, int J, const double *lambda, c
     HQB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     hqb::k_batch_dispatch<<<nsm * 8, 256, 0, s>>>(a, d_Wd);
     HQB_CUDA(cudaGetLastError());
-    const size_t sm = sizeof(double) * 5 * S;
+    for (int n = 0; n <= N; n++) a.maxc = std::max(a.maxc, a.off[n + 1] - a.off[n]);
+    const size_t sm = sizeof(double) * (3 * (size_t)S + 2 * (size_t)a.maxc);
     HQB_CUDA(cudaFuncSetAttribute(hqb::k_batch_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     int per_sm = 1;
-    HQB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hqb::k_batch_solve, hqb::kThreads, sm));
+    const int nthr = S <= 1024 ? 128 : hqb::kThreads;   // small state spaces: more, smaller CTAs (measured)
+    HQB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hqb::k_batch_solve, nthr, sm));
     const int grid = std::min(B, nsm * std::max(1, per_sm));
-    hqb::k_batch_solve<<<grid, hqb::kThreads, sm, s>>>(a);
+    hqb::k_batch_solve<<<grid, nthr, sm, s>>>(a);
     HQB_CUDA(cudaGetLastError());
     std::vector<int> it(B), er(B);
     std::vector<double> rr(B);
