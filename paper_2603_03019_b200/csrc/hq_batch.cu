@@ -405,7 +405,7 @@ extern "C" hq_status hq_batch_solve(int B, int N, int J, const double *lambda, c
     const size_t sm = sizeof(double) * (3 * (size_t)S + 2 * (size_t)a.maxc);
     HQB_CUDA(cudaFuncSetAttribute(hqb::k_batch_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     int per_sm = 1;
-    const int nthr = S <= 1024 ? 128 : hqb::kThreads;   // small state spaces: more, smaller CTAs (measured)
+    const int nthr = S <= 256 ? 64 : S <= 1024 ? 128 : hqb::kThreads;   // small state spaces: more, smaller CTAs (measured)
     HQB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hqb::k_batch_solve, nthr, sm));
     const int grid = std::min(B, nsm * std::max(1, per_sm));
     hqb::k_batch_solve<<<grid, nthr, sm, s>>>(a);
