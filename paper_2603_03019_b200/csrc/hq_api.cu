@@ -889,9 +889,15 @@ static hq_status v3_programs(hq_problem *h, cudaStream_t s, int nwv, const std::
     p3.lam_thr = h->d_lthr;
     p3.lam_end = h->d_lend;
     const int g = h->nsm * 8;
-    // pair cache for the write pass: up to 256 MB, at most 512 pairs per program
+    // pair cache for the write pass: a quarter of the free device memory (256 MB .. 2 GB),
+    // at most 512 pairs per program
     {
-        const uint64_t budget = 256ull << 20;
+        size_t fr = 0, tot = 0;
+        if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
+            cudaGetLastError();
+            fr = 0;
+        }
+        const uint64_t budget = std::min<uint64_t>(2ull << 30, std::max<uint64_t>(256ull << 20, fr / 4));
         const int64_t per = (int64_t)(budget / nprog) - 32 * 8;
         const int ccap = (int)std::min<int64_t>(512, per > 0 ? per / 14 : 0);
         if (ccap >= 32 && dmalloc(&cache, nprog * ((size_t)ccap * 14 + 32 * 8 + 4)) == cudaSuccess) {
