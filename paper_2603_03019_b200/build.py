@@ -33,6 +33,7 @@ def build(force: bool = False, verbose: bool = False, out: str = None, defines=(
         nvcc = os.environ.get("NVCC", "nvcc")
         extra = ["-DHQ_DEBUG_HANG"] if os.environ.get("HQ_DEBUG_HANG") else []
         extra += ["-D" + d for d in defines]
+        extra += os.environ.get("HQ_NVCC_EXTRA", "").split()   # development: extra nvcc flags
         cmd = [nvcc] + NVCC_FLAGS + extra + (["-Xptxas", "-v"] if verbose else []) + ["-o", lib] + SOURCES
         subprocess.run(cmd, check=True)
     return lib
