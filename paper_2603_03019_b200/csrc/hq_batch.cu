@@ -304,9 +304,9 @@ extern "C" hq_status hq_batch_solve(int B, int N, int J, const double *lambda, c
         if (!(L > 0.0)) return batch_fail("instance " + std::to_string(b) + ": sum of lambda must be > 0");
         for (int i = 0; i < N; i++)
             if (!std::isfinite(nu[i]) || !(nu[i] > 0.0)) return batch_fail("instance " + std::to_string(b) + ": mu");
-        std::vector<char> reach(N, 0);
+        char reach[hqb::kMaxN] = {0};
         for (int j = 0; j < J; j++) {
-            std::vector<char> seen(N, 0);
+            char seen[hqb::kMaxN] = {0};
             bool ended = false;
             int len = 0;
             for (int h = 0; h < N; h++) {
