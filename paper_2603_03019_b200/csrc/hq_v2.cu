@@ -669,7 +669,7 @@ __global__ void __launch_bounds__(1024) k_scalars2(int N, int full_lists, double
     const int lane = threadIdx.x & 31, n = threadIdx.x >> 5;
     for (int i = threadIdx.x; i < V2S_TOTAL; i += blockDim.x) sblk[i] = blk[i];
     if (transposed) {   // partial[(layer * HQ_NV + v) * ncta + cta]
-        reduce_partials_t(partial, ncta, N, S, 5);   // one warp per (layer, value)
+        reduce_partials_t(partial, ncta, N, S, 5, mode == 1 ? active : 0u);   // one warp per (layer, value)
     } else if (n <= N) {
         double s[NV2];
 #pragma unroll
