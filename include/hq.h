@@ -232,8 +232,9 @@ const char *hq_error_string(hq_handle h);
  *   [14] largest rate-program block of a CTA tile (16-byte records),
  *   [15] warp bits varying inside a rate program (0: one program per warp tile,
  *        the default; nW: one program per CTA tile, HQ_PROG=cta),
- *   [16], [17] timed sweep launches (ms) with CTA / warp programs at that choice
- *        (0: not timed).
+ *   [16], [17] reserved (0),
+ *   [18] tile visit order of the CTA-tiled path: -1 popcount order, b >= 0 chunked
+ *        order with chunks of 2^b tiles (N >= 27).
  */
 #define HQ_STATS_LEN 20
 hq_status hq_stats(hq_handle h, double *out);

@@ -1,6 +1,7 @@
 """Build libhq.so (the C-ABI library) in-tree with nvcc for sm_100a."""
 from __future__ import annotations
 
+import concurrent.futures
 import glob
 import os
 import subprocess
@@ -34,8 +35,17 @@ def build(force: bool = False, verbose: bool = False, out: str = None, defines=(
         extra = ["-DHQ_DEBUG_HANG"] if os.environ.get("HQ_DEBUG_HANG") else []
         extra += ["-D" + d for d in defines]
         extra += os.environ.get("HQ_NVCC_EXTRA", "").split()   # development: extra nvcc flags
-        cmd = [nvcc] + NVCC_FLAGS + extra + (["-Xptxas", "-v"] if verbose else []) + ["-o", lib] + SOURCES
-        subprocess.run(cmd, check=True)
+        # one object per translation unit, compiled in parallel, then one shared-library link
+        flags = [f for f in NVCC_FLAGS if f != "-shared"] + extra + (["-Xptxas", "-v"] if verbose else [])
+        objdir = os.path.join(PKG, "build", os.path.basename(lib) + ".o")
+        os.makedirs(objdir, exist_ok=True)
+        objs = [os.path.join(objdir, os.path.basename(src)[:-3] + ".o") for src in SOURCES]
+        with concurrent.futures.ThreadPoolExecutor(len(SOURCES)) as ex:
+            futs = [ex.submit(subprocess.run, [nvcc] + flags + ["-c", "-o", o, src], check=True)
+                    for src, o in zip(SOURCES, objs)]
+            for f in futs:
+                f.result()
+        subprocess.run([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", lib] + objs, check=True)
     return lib
 
 

@@ -348,6 +348,7 @@ struct hq_problem {
     std::vector<double> nu_int;    // service rates in internal order
     std::string err;
     int device = -1;
+    bool dev_ready = false;        // every per-device buffer of `device` allocated and filled
     int nsm = 0;
     bool solved = false;
     // waiting room (hq_set_buffer): 0 loss system, C > 0 finite buffer, -1 unlimited
@@ -379,6 +380,9 @@ struct hq_problem {
     uint32_t maxblk_all = 0;       // path 3: largest program block of a CTA tile (records)
     unsigned long long *d_wtime = nullptr;   // path 3: per-warp busy cycles (-DHQ_WARP_TIMING builds)
     int prog_nwv = 0;              // path 3: warp bits varying inside a rate program (nW: CTA programs)
+    bool chunked = false;          // path 3: chunked tile order (else popcount order)
+    int chunk_bits = 0;            // path 3, chunked order: low tile bits per chunk
+    std::vector<uint32_t> chunk_range;   // path 3, chunked order: CTA ranges over the visit order
     float tune_ms[2] = {0.f, 0.f}; // path 3: timed sweeps with CTA / warp programs (0: not tuned)
     uint32_t *d_order = nullptr, *d_off16 = nullptr, *d_size16 = nullptr, *d_range = nullptr;
     uint4 *d_prog = nullptr;
@@ -399,10 +403,7 @@ struct hq_problem {
         return ev[i];
     }
 
-    ~hq_problem() {
-        release();
-        for (auto e : ev) cudaEventDestroy(e);
-    }
+    ~hq_problem() { release(); }
     void release() {
         dfree(d_node);
         dfree(d_lthr);
@@ -428,12 +429,17 @@ struct hq_problem {
         if (side) cudaStreamDestroy(side);
         if (ev_fork) cudaEventDestroy(ev_fork);
         if (ev_join) cudaEventDestroy(ev_join);
+        side = nullptr;
+        ev_fork = ev_join = nullptr;
+        for (auto e : ev) cudaEventDestroy(e);   // events belong to the device they were created on
+        ev.clear();
         pinned_free(h_blk, sizeof(double) * V2S_TOTAL);
         d_order = d_off16 = d_size16 = nullptr;
         d_prog = nullptr;
         d_omkap = nullptr;
         d_lamarr = d_blk = h_blk = nullptr;
         v2_ready = false;
+        dev_ready = false;
         pinned_free(h_small, sizeof(double) * S_TOTAL);
         d_node = nullptr;
         d_lthr = d_lend = d_lam = nullptr;
@@ -537,6 +543,8 @@ extern "C" hq_status hq_create(int N, int J, const double *lambda, const double 
     return HQ_OK;
 }
 
+static hq_status alloc_device(hq_problem *h);
+
 static hq_status ensure_device(hq_problem *h) {
     int dev = -1;
     cudaError_t e = cudaGetDevice(&dev);
@@ -544,9 +552,22 @@ static hq_status ensure_device(hq_problem *h) {
         h->err = std::string("no CUDA device: ") + cudaGetErrorString(e);
         return HQ_E_CUDA;
     }
-    if (h->device == dev && h->d_pw) return HQ_OK;
-    if (h->device != -1 && h->device != dev) h->release();
+    if (h->device == dev && h->dev_ready) return HQ_OK;
+    if (h->device != -1) h->release();   // other device, or a partial set from a failed call
     h->device = dev;
+    const hq_status st = alloc_device(h);
+    if (st != HQ_OK) {   // never keep a partial buffer set: the next call starts over
+        cudaGetLastError();
+        h->release();
+        h->device = -1;
+        return st;
+    }
+    h->dev_ready = true;
+    return HQ_OK;
+}
+
+static hq_status alloc_device(hq_problem *h) {
+    const int dev = h->device;
     HQ_CUDA(cudaDeviceGetAttribute(&h->nsm, cudaDevAttrMultiProcessorCount, dev));
     const int N = h->N;
     const size_t S = (size_t)1 << N;
@@ -563,9 +584,6 @@ static hq_status ensure_device(hq_problem *h) {
     if (alloc((void **)&h->d_pw, sizeof(double) * S) != cudaSuccess ||
         (!h->v2 && alloc((void **)&h->d_ab, sizeof(double2) * (S >> 1 ? S >> 1 : 1)) != cudaSuccess) ||
         (h->v2 && alloc((void **)&h->d_omkap, sizeof(double2) * S) != cudaSuccess)) {
-        cudaGetLastError();
-        h->release();
-        h->device = -1;
         h->err = "device memory for the working set (2^N doubles x 2) could not be allocated";
         return HQ_E_NOMEM;
     }
@@ -1003,6 +1021,7 @@ static hq_status v3_programs(hq_problem *h, cudaStream_t s, int nwv, const std::
         else lo = mid;
     }
     pack(hi, &range);
+    if (h->chunked) range = h->chunk_range;   // chunked order: each CTA's own chunks
     HQ_CUDA(dmalloc((void **)&ps.range, 4 * (G + 1)));
     HQ_CUDA(cudaMemcpyAsync(ps.range, range.data(), 4 * (G + 1), cudaMemcpyHostToDevice, s));
     HQ_CUDA(cudaMemcpyAsync(&herr, h->d_err, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -1046,42 +1065,63 @@ static cudaError_t tiled_sweep(hq_problem *h, const S2Args &sa, int mode, cudaSt
                                const FoldArgs *f = nullptr);
 static S2Args base_s2(hq_problem *h);
 
-// time MODE-0 sweep launches with the programs now installed (the iterate is garbage:
-// timing only; hq_solve re-initialises everything afterwards)
-static hq_status v3_time_sweep(hq_problem *h, cudaStream_t s, float *ms) {
-    S2Args sa = base_s2(h);
-    const uint64_t half = 1ull << (h->N - 1);
-    sa.c = 1;
-    sa.active = 0xaaaaaaaau & ((1u << h->N) - 2u);
-    sa.P = h->d_pw + half;
-    sa.Q = h->d_pw;
-    sa.omkap = h->d_omkap + half;
-    cudaEvent_t e0 = h->event(0), e1 = h->event(1);
-    HQ_CUDA(tiled_sweep(h, sa, 0, s));
-    HQ_CUDA(cudaEventRecord(e0, s));
-    for (int i = 0; i < 2; i++) HQ_CUDA(tiled_sweep(h, sa, 0, s));
-    HQ_CUDA(cudaEventRecord(e1, s));
-    HQ_CUDA(cudaEventSynchronize(e1));
-    cudaEventElapsedTime(ms, e0, e1);
-    return HQ_OK;
-}
-
 static hq_status v3_prepare(hq_problem *h, cudaStream_t s) {
     if (h->v2_ready) return HQ_OK;
     const int N = h->N;
     const uint64_t S = 1ull << N;
     const int Nt = N - 9 - h->nW;
     const uint64_t ntiles = 1ull << Nt;
-    // CTA tile visit order: by popcount of the tile index, ascending within a popcount class
+    // CTA tile visit order (DESIGN.md §4 "Tile order").
+    //  * popcount order (N < 27): tiles by popcount of the tile index; every CTA takes a
+    //    contiguous, work-balanced range of it.  A popcount class of q blocks fits in L2 up to
+    //    N = 26, so the tile-unit neighbours of the tiles in flight are L2 hits.
+    //  * chunked order (N >= 27): "chunks" = sub-cubes of the b low tile bits (the high tile
+    //    bits fixed); chunk k goes to CTA k mod G, so at any time the CTAs work on G
+    //    consecutive chunks and a neighbour along a high tile bit h was read about 2^h / G
+    //    chunk steps earlier (an L2 hit while that distance stays inside the L2 window); the
+    //    tiles of a chunk follow the popcount of their low bits (b + 1 layer-bin flushes per
+    //    chunk).  Each CTA's chunks are contiguous in `order`, its range is exactly them.
     std::vector<uint32_t> order;
     order.reserve(ntiles);
-    order.push_back(0);
-    for (int K = 1; K <= Nt; K++) {
-        uint64_t x = (1ull << K) - 1;
-        while (x < ntiles) {
-            order.push_back((uint32_t)x);
-            const uint64_t cc = x & (~x + 1), r = x + cc;
-            x = (((r ^ x) >> 2) / cc) | r;
+    auto popcount_order = [](int bits, std::vector<uint32_t> &out) {
+        out.push_back(0);
+        for (int K = 1; K <= bits; K++) {
+            uint64_t x = (1ull << K) - 1;
+            while (x < (1ull << bits)) {
+                out.push_back((uint32_t)x);
+                const uint64_t cc = x & (~x + 1), r = x + cc;
+                x = (((r ^ x) >> 2) / cc) | r;
+            }
+        }
+    };
+    h->chunk_bits = 0;
+    h->chunked = false;
+    {
+        const char *oenv = getenv("HQ_ORDER");
+        const std::string om = oenv ? oenv : "";
+        bool chunked = N >= 27;
+        if (om == "popcount") chunked = false;
+        if (om == "chunk") chunked = true;
+        int b = 3;
+        if (const char *benv = getenv("HQ_CHUNK_BITS")) b = atoi(benv);
+        b = std::max(0, std::min(b, Nt));
+        if (chunked && ((ntiles >> b) < (uint64_t)h->sgrid)) chunked = false;   // too few chunks to spread
+        if (chunked) {
+            h->chunk_bits = b;
+            h->chunked = true;
+            std::vector<uint32_t> low;
+            popcount_order(b, low);
+            const uint64_t nch = ntiles >> b;
+            const int G = h->sgrid;
+            h->chunk_range.assign(G + 1, 0);
+            for (int cta = 0; cta < G; cta++) {
+                h->chunk_range[cta] = (uint32_t)order.size();
+                for (uint64_t k = (uint64_t)cta; k < nch; k += (uint64_t)G)
+                    for (uint32_t lo : low) order.push_back((uint32_t)(k << b) | lo);
+            }
+            h->chunk_range[G] = (uint32_t)order.size();
+        } else {
+            popcount_order(Nt, order);
         }
     }
     if (dmalloc((void **)&h->d_order, 4 * ntiles) != cudaSuccess ||
@@ -1117,66 +1157,12 @@ static hq_status v3_prepare(hq_problem *h, cudaStream_t s) {
     HQ_CUDA(hq2_launch::omkap(pa, h->d_lamarr, h->d_omkap, g, h->side));
     HQ_CUDA(cudaEventRecord(h->ev_join, h->side));
     // program granularity: warp programs (warp bits folded; fewer pairs per thread; the
-    // default) or CTA programs (warps share one program).  HQ_PROG=cta forces CTA programs;
-    // HQ_PROG=auto builds both and keeps the faster sweep (timing-dependent, so results may
-    // differ bitwise between handles -- development only; the default is deterministic).
+    // default) or CTA programs (warps share one program; HQ_PROG=cta, development A/B).
     const char *env = getenv("HQ_PROG");
-    const std::string pref = env ? env : "warp";
-    ProgSet a, b;
-    hq_status st;
-    if (pref != "cta" && pref != "auto") {
-        st = v3_programs(h, s, 0, order, a);
-        if (st != HQ_OK) return st;
-    } else if (pref == "cta" || h->nW == 0) {
-        st = v3_programs(h, s, h->nW, order, a);
-        if (st != HQ_OK) return st;
-    } else {
-        HQ_CUDA(cudaStreamWaitEvent(s, h->ev_join, 0));   // the timed sweeps read omega/kappa
-        float tc = INFINITY, tw = INFINITY;
-        st = v3_programs(h, s, h->nW, order, a);
-        if (st == HQ_OK) {
-            use_progset(h, a);
-            st = v3_time_sweep(h, s, &tc);
-            if (st != HQ_OK) return st;
-        } else if (st != HQ_E_NUMERIC) {
-            return st;
-        }
-        st = v3_programs(h, s, 0, order, b);
-        if (st != HQ_OK) return st;
-        if (std::isfinite(tc)) {
-            ProgSet cur;   // take back the CTA set
-            cur.off16 = h->d_off16;
-            cur.range = h->d_range;
-            cur.prog = h->d_prog;
-            cur.total16 = h->total16;
-            cur.maxblk = h->maxblk_all;
-            cur.cap = h->maxrec;
-            cur.nwv = h->prog_nwv;
-            h->d_off16 = nullptr;
-            h->d_range = nullptr;
-            h->d_prog = nullptr;
-            use_progset(h, b);
-            st = v3_time_sweep(h, s, &tw);
-            if (st != HQ_OK) return st;
-            h->tune_ms[0] = tc;
-            h->tune_ms[1] = tw;
-            if (tc < tw) {
-                ProgSet w;
-                w.off16 = h->d_off16;
-                w.range = h->d_range;
-                w.prog = h->d_prog;
-                h->d_off16 = nullptr;
-                h->d_range = nullptr;
-                h->d_prog = nullptr;
-                w.release();
-                use_progset(h, cur);
-            } else {
-                cur.release();
-            }
-        }
-        a = ProgSet();
-        b = ProgSet();
-    }
+    const bool cta_prog = env && std::string(env) == "cta";
+    ProgSet a;
+    hq_status st = v3_programs(h, s, cta_prog ? h->nW : 0, order, a);
+    if (st != HQ_OK) return st;
     if (a.prog) use_progset(h, a);
     h->nslots = hq3_launch::choose_slots(h->nW, h->maxrec);
     if (h->nslots < 1) {
@@ -1420,6 +1406,12 @@ static hq_status solve_v2(hq_problem *h, double tol, int max_iter, double *pi, c
         if (st != HQ_OK) return st;
         if (tol > 0.0 && o.res <= tol) o.converged = true;
     }
+    // the sticky error flag of the scalar steps (v2_residual copied the block to the host):
+    // checked on every exit, not only at scheduled convergence checks
+    if (h->h_blk[V2S_MISC + 0] != 0.0) {
+        h->err = "non-positive or non-finite layer normaliser";
+        return HQ_E_NUMERIC;
+    }
     HQ_CUDA(hq2_launch::assemble(N, h->d_pw, h->d_blk + V2S_PN, h->perm.data(), pi, h->nsm * 8, s));
     o.launches++;
     // layer masses for the stats
@@ -1489,6 +1481,7 @@ static hq_status solve_core(hq_handle h, double tol, int max_iter, double *pi, v
         h->stats[15] = h->prog_nwv;
         h->stats[16] = h->tune_ms[0];
         h->stats[17] = h->tune_ms[1];
+        h->stats[18] = h->chunked ? h->chunk_bits : -1;
         if (iters_out) *iters_out = o.sweeps;
         if (residual_out) *residual_out = o.res;
         if (!std::isfinite(o.res)) {

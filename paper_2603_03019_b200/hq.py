@@ -30,6 +30,7 @@ HQ_BUFFER_UNLIMITED = -1
 
 _dptr = ctypes.POINTER(ctypes.c_double)
 _lib = None
+_dims = {}   # handle -> (N, J), recorded by hq_create for the binding's size checks
 
 
 class HQError(RuntimeError):
@@ -99,7 +100,13 @@ def hq_create(N, J, lam, mu, pref):
                        pref.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), ctypes.byref(h))
     if st != HQ_OK:
         raise HQError(st, lib.hq_error_string(None).decode())
+    _dims[h.value] = (int(N), int(J))
     return h.value
+
+
+def _check_size(t, n, what):
+    if t.numel() != n:
+        raise HQError(HQ_E_INVAL, f"{what} must have {n} elements, got {t.numel()}")
 
 
 def _stream_ptr(stream):
@@ -115,6 +122,8 @@ def hq_solve(h, tol, max_iter, pi, stream=None):
     (status, iters, residual); raises on errors (status < 0)."""
     lib = load()
     _check_tensor(pi)
+    if h in _dims:
+        _check_size(pi, 1 << _dims[h][0], "pi")
     it = ctypes.c_int(0)
     res = ctypes.c_double(0.0)
     st = lib.hq_solve(ctypes.c_void_p(h), float(tol), int(max_iter), ctypes.c_void_p(pi.data_ptr()),
@@ -128,6 +137,11 @@ def hq_measures(h, pi, workload, dispatch, stream=None):
     lib = load()
     for t in (pi, workload, dispatch):
         _check_tensor(t)
+    if h in _dims:
+        N, J = _dims[h]
+        _check_size(pi, 1 << N, "pi")
+        _check_size(workload, N, "workload")
+        _check_size(dispatch, J * N, "dispatch")
     loss = ctypes.c_double(0.0)
     st = lib.hq_measures(ctypes.c_void_p(h), ctypes.c_void_p(pi.data_ptr()), ctypes.c_void_p(workload.data_ptr()),
                          ctypes.c_void_p(dispatch.data_ptr()), ctypes.byref(loss), _stream_ptr(stream))
@@ -173,6 +187,7 @@ def hq_batch_solve(lam, mu, pref, tol=1e-13, max_iter=10000, pi=None, stream=Non
     if pi is None:
         pi = torch.empty((B, 1 << N), dtype=torch.float64, device="cuda")
     _check_tensor(pi)
+    _check_size(pi, B << N, "pi")
     it = np.zeros(B, dtype=np.int32)
     res = np.zeros(B)
     sts = np.zeros(B, dtype=np.int32)
@@ -200,6 +215,14 @@ def hq_response_times(h, dispatch, tau, T_bar, mrt_j=None, f_j=None, stream=None
     lib = load()
     _check_tensor(dispatch)
     tau = np.ascontiguousarray(tau, dtype=np.float64)
+    if h in _dims:
+        N, J = _dims[h]
+        _check_size(dispatch, J * N, "dispatch")
+        if tau.shape != (J, N):
+            raise HQError(HQ_E_INVAL, f"tau must have shape ({J}, {N}), got {tau.shape}")
+        for t in (mrt_j, f_j):
+            if t is not None:
+                _check_size(t, J, "per-atom output")
     mrt = ctypes.c_double(0.0)
     frac = ctypes.c_double(0.0)
     ptr = lambda t: ctypes.c_void_p(t.data_ptr()) if t is not None else None  # noqa: E731
@@ -216,6 +239,7 @@ def hq_response_times(h, dispatch, tau, T_bar, mrt_j=None, f_j=None, stream=None
 
 def hq_destroy(h):
     if h:
+        _dims.pop(h, None)
         load().hq_destroy(ctypes.c_void_p(h))
 
 
@@ -297,7 +321,7 @@ class Solver:
         s = hq_stats(self.h)
         keys = ["sweeps", "halfsweeps", "state_updates", "launches", "residual_evals", "trie_nodes", "sum_pi_minus_1",
                 "solve_ms", "sweep_ms", "sweep_launches", "residual_ms", "precompute_ms", "program_bytes", "path",
-                "max_program_block", "program_nwv", "tune_ms_cta", "tune_ms_warp"]
+                "max_program_block", "program_nwv", "reserved16", "reserved17", "chunk_bits"]
         return {k: float(s[i]) for i, k in enumerate(keys)}
 
     def close(self):

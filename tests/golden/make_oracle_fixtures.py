@@ -8,6 +8,7 @@ sweeps and residual, the layer masses, the measures, and pi at a seeded
 sample of states (every state of the three lowest and three highest layers,
 plus uniform random states).
 """
+import itertools
 import os
 import sys
 import time
@@ -21,17 +22,41 @@ import hqinst  # noqa: E402
 import oracle  # noqa: E402
 
 
+def edge_states(N):
+    """every state of the layers 0, 1, 2, N-2, N-1, N (enumerated by combinations)"""
+    full = (1 << N) - 1
+    low = [0] + [1 << a for a in range(N)] + [(1 << a) | (1 << b) for a, b in itertools.combinations(range(N), 2)]
+    return sorted(set(low) | {full ^ m for m in low})
+
+
 def sample_states(N, nrand=6000, seed=123):
     rng = np.random.default_rng(seed)
     S = 1 << N
-    edge = [m for m in range(S) if bin(m).count("1") in (0, 1, 2, N - 2, N - 1, N)] if N <= 26 else []
+    if N <= 26:
+        edge = [m for m in range(S) if bin(m).count("1") in (0, 1, 2, N - 2, N - 1, N)]
+    else:
+        edge = edge_states(N)
     rnd = rng.integers(0, S, size=nrand)
     return np.unique(np.concatenate([np.array(edge, dtype=np.int64), rnd.astype(np.int64)]))
 
 
+def popcounts(N):
+    idx = np.arange(1 << N, dtype=np.uint32)
+    pc = np.zeros(1 << N, dtype=np.int8)
+    tab = np.array([bin(b).count("1") for b in range(256)], dtype=np.int8)
+    for sh in range(0, 32, 8):
+        pc += tab[(idx >> sh) & 0xFF]
+    return pc
+
+
 def main(which):
+    extra = {}
     if which == "cfg3":
         inst = hqinst.config_instance(3)
+        nrand = 6000
+    elif which == "cfg4":
+        inst = hqinst.config_instance(4)
+        nrand = 20000
     else:
         raise SystemExit("unknown fixture " + which)
     t = time.time()
@@ -39,20 +64,20 @@ def main(which):
     dt = time.time() - t
     pi = r["pi"]
     N = inst.N
-    pc = np.array([bin(m).count("1") for m in range(1 << N)], dtype=np.int64) if N <= 20 else None
-    if pc is None:
-        # popcount by bytes
-        idx = np.arange(1 << N, dtype=np.uint32)
-        pc = np.zeros(1 << N, dtype=np.int64)
-        for sh in range(0, 32, 8):
-            pc += np.array([bin(b).count("1") for b in range(256)], dtype=np.int64)[(idx >> sh) & 0xFF]
+    pc = popcounts(N)
     masses = np.bincount(pc, weights=pi, minlength=N + 1)
+    del pc
+    if N >= 26:
+        # sums of pi over consecutive blocks of 2^14 natural indices (whole-vector check at
+        # sizes whose pi is too large to commit), in ascending order within a block
+        extra["block_bits"] = 14
+        extra["block_sums"] = pi.reshape(-1, 1 << 14).sum(axis=1)
     w, d, loss = oracle.measures(inst, pi)
-    st = sample_states(N)
+    st = sample_states(N, nrand=nrand)
     out = os.path.join(HERE, f"oracle_{which}.npz")
     np.savez_compressed(out, sha256=inst.sha256(), iters=r["iters"], residual=r["residual"], status=r["status"],
                         masses=masses, workload=w, dispatch=d, loss=loss, states=st, pi_states=pi[st],
-                        oracle_seconds=dt, oracle_threads=oracle.num_threads(), tol=1e-13)
+                        oracle_seconds=dt, oracle_threads=oracle.num_threads(), tol=1e-13, **extra)
     print(f"wrote {out}: iters={r['iters']} residual={r['residual']:.3e} time={dt:.1f}s threads={oracle.num_threads()}")
 
 

@@ -28,7 +28,7 @@ import json, os, statistics, sys
 sys.path.insert(0, os.environ["ROOT"])
 import torch, hqinst
 from paper_2603_03019_b200 import hq
-inst = hqinst.config_instance(int(os.environ["CFG"]))
+inst = hqinst.config_instance(int(os.environ["CFG"]), rho=float(os.environ["RHO"]) if os.environ.get("RHO") else None)
 s = hq.Solver.from_instance(inst)
 pi = torch.empty(1 << inst.N, dtype=torch.float64, device="cuda")
 for _ in range(2):
@@ -38,7 +38,7 @@ for _ in range(int(os.environ["REPS"])):
     r = s.solve(tol=1e-13, max_iter=5000, pi=pi)
     st = s.stats()
     out.append((st["solve_ms"], st["sweep_ms"], r["iters"], r["residual"], st.get("program_nwv", -1),
-                st.get("tune_ms_cta", 0), st.get("tune_ms_warp", 0)))
+                st.get("chunk_bits", -1), 0))
 print(json.dumps(out))
 '''
 res = {n: [] for n in names}
@@ -46,7 +46,9 @@ for rnd in range(2):   # two interleaved rounds of fresh processes
     for n in names:
         # NAME@cta / NAME@warp forces the program granularity; NAME@VAR=VALUE sets an env var
         lib, *mods = n.split("@")
-        env = dict(os.environ, ROOT=ROOT, CFG=str(cfg), REPS=str(reps), HQ_LIB=os.path.join(VAR, f"libhq_{lib}.so"))
+        libpath = os.path.join(ROOT, "paper_2603_03019_b200", "libhq.so") if lib == "main" else \
+            os.path.join(VAR, f"libhq_{lib}.so")
+        env = dict(os.environ, ROOT=ROOT, CFG=str(cfg), REPS=str(reps), HQ_LIB=libpath)
         for mod in mods:
             k, eq, v = mod.partition("=")
             if eq:
