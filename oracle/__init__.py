@@ -44,9 +44,11 @@ _u64ptr = ctypes.POINTER(ctypes.c_uint64)
 def build(force: bool = False) -> str:
     """Compile hq_oracle.c into liboracle.so (gcc, -O2, OpenMP, no fast-math)."""
     if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC):
+        tmp = _LIB_PATH + f".tmp{os.getpid()}"
         cmd = ["gcc", "-O2", "-fopenmp", "-fno-fast-math", "-ffp-contract=off", "-shared", "-fPIC",
-               "-std=c11", "-Wall", "-o", _LIB_PATH, _SRC, "-lm"]
+               "-std=c11", "-Wall", "-o", tmp, _SRC, "-lm"]
         subprocess.run(cmd, check=True)
+        os.replace(tmp, _LIB_PATH)   # new inode: a process that has the old library loaded keeps it
     return _LIB_PATH
 
 
@@ -73,6 +75,13 @@ def _load():
             lib.oracle_state_balance.restype = ctypes.c_int
             lib.oracle_state_balance.argtypes = [ctypes.c_int, ctypes.c_int, _dptr, _dptr, _iptr, _u64ptr,
                                                  ctypes.c_int64, _dptr, _dptr]
+            lib.oracle_residual_stream.restype = ctypes.c_double
+            lib.oracle_residual_stream.argtypes = [ctypes.c_int, ctypes.c_int, _dptr, _dptr, _iptr, _dptr,
+                                                   ctypes.c_int, _dptr, _dptr]
+            lib.oracle_tree_rates.restype = ctypes.c_double
+            lib.oracle_tree_rates.argtypes = [ctypes.c_int, ctypes.c_int, _dptr, _iptr, ctypes.c_uint64, _dptr]
+            lib.oracle_lambda_m.restype = ctypes.c_double
+            lib.oracle_lambda_m.argtypes = [ctypes.c_int, ctypes.c_int, _dptr, _iptr, ctypes.c_uint64]
             lib.oracle_num_threads.restype = ctypes.c_int
             _lib = lib
     return _lib
@@ -124,6 +133,36 @@ def residual(inst, pi) -> float:
     pi = np.ascontiguousarray(pi, dtype=np.float64)
     assert pi.shape == (1 << inst.N,)
     return float(lib.oracle_residual(inst.N, inst.J, _d(lam), _d(mu), pref.ctypes.data_as(_iptr), _d(pi)))
+
+
+def residual_stream(inst, pi, block_bits: int = 16):
+    """r(pi) like ``residual`` with O(2^N / 2^block_bits) scratch (rates through the
+    prefix tree of the lists; fixed-order block sums).  Returns (r, num, den)."""
+    lib = _load()
+    lam, mu, pref = _arrays(inst)
+    pi = np.ascontiguousarray(pi, dtype=np.float64)
+    assert pi.shape == (1 << inst.N,)
+    num = ctypes.c_double(0.0)
+    den = ctypes.c_double(0.0)
+    r = lib.oracle_residual_stream(inst.N, inst.J, _d(lam), _d(mu), pref.ctypes.data_as(_iptr), _d(pi),
+                                   int(block_bits), ctypes.byref(num), ctypes.byref(den))
+    return float(r), num.value, den.value
+
+
+def tree_rates(inst, m: int):
+    """(W[N], lambda_m) of state m through the oracle's prefix tree."""
+    lib = _load()
+    lam, _, pref = _arrays(inst)
+    W = np.zeros(inst.N)
+    lm = lib.oracle_tree_rates(inst.N, inst.J, _d(lam), pref.ctypes.data_as(_iptr), int(m), _d(W))
+    return W, float(lm)
+
+
+def lambda_m(inst, m: int) -> float:
+    """lambda_m by list scans (Table 1)."""
+    lib = _load()
+    lam, _, pref = _arrays(inst)
+    return float(lib.oracle_lambda_m(inst.N, inst.J, _d(lam), pref.ctypes.data_as(_iptr), int(m)))
 
 
 def measures(inst, pi):

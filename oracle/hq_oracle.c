@@ -42,6 +42,9 @@
  *   oracle_measures         utilisation rho_i, dispatch
  *                           fractions rho_ij over S_ij and Pi
  *                           (PAPER.md:787-789, 1759-1761), readings C12, C13.
+ *   oracle_residual_stream  the same residual with O(2^N / 2^B) scratch and the
+ *                           rates of Eq. tran_rates taken through a prefix tree of
+ *                           the lists (full-size checks, N up to 31).
  *   oracle_state_balance    the same balance equation at caller-chosen states
  *                           (sampled parity checks at sizes where a full
  *                           oracle run is infeasible).
@@ -406,6 +409,150 @@ double oracle_residual(int N, int J, const double *lam, const double *mu, const 
     inst_t I = {N, J, lam, mu, pref};
     rates_t R = {&I, NULL, NULL, NULL};
     return residual(&R, pi);
+}
+
+/* ---------------------------------------------------------------------- */
+/* Memory-lean residual (full-size checks)                                 */
+/* ---------------------------------------------------------------------- */
+
+/* Prefix tree of the preference lists: one node per distinct list prefix
+ * zeta_j(1..h); thr[v] = sum of lam_j over the atoms whose list starts with
+ * that prefix.  Children are kept as a first-child / next-sibling list. */
+typedef struct {
+    int n, cap;
+    int *unit, *child, *sib;
+    double *thr;
+} ptree_t;
+
+static int ptree_node(ptree_t *T, int unit) {
+    if (T->n == T->cap) {
+        T->cap = T->cap ? 2 * T->cap : 1024;
+        T->unit = (int *)realloc(T->unit, sizeof(int) * T->cap);
+        T->child = (int *)realloc(T->child, sizeof(int) * T->cap);
+        T->sib = (int *)realloc(T->sib, sizeof(int) * T->cap);
+        T->thr = (double *)realloc(T->thr, sizeof(double) * T->cap);
+    }
+    T->unit[T->n] = unit;
+    T->child[T->n] = -1;
+    T->sib[T->n] = -1;
+    T->thr[T->n] = 0.0;
+    return T->n++;
+}
+
+static void ptree_build(const inst_t *I, ptree_t *T) {
+    memset(T, 0, sizeof(*T));
+    ptree_node(T, -1);   /* root: the empty prefix */
+    for (int j = 0; j < I->J; j++) {
+        int cur = 0;
+        for (int h = 0; h < I->N; h++) {
+            int u = I->pref[(size_t)j * I->N + h];
+            if (u < 0) break;
+            int c = T->child[cur];
+            while (c >= 0 && T->unit[c] != u) c = T->sib[c];
+            if (c < 0) {
+                c = ptree_node(T, u);
+                T->sib[c] = T->child[cur];
+                T->child[cur] = c;
+            }
+            T->thr[c] += I->lam[j];
+            cur = c;
+        }
+    }
+}
+
+static void ptree_free(ptree_t *T) { free(T->unit); free(T->child); free(T->sib); free(T->thr); }
+
+/* Eq. tran_rates at state m through the prefix tree (readings C6, C19): the
+ * atoms through a node whose units are all busy in m reach its children; a
+ * child whose unit i is busy receives them as the upward rate W[i] =
+ * lambda_{m\i -> m}; a free child's unit is their first free unit, so they
+ * count in lambda_m; atoms whose whole list is busy are lost (C = 0). */
+static double ptree_rates(const ptree_t *T, int N, uint64_t m, double *W, int *stk) {
+    for (int i = 0; i < N; i++) W[i] = 0.0;
+    double lm = 0.0;
+    int sp = 0;
+    stk[sp++] = 0;
+    while (sp > 0) {
+        int v = stk[--sp];
+        for (int c = T->child[v]; c >= 0; c = T->sib[c]) {
+            int u = T->unit[c];
+            if ((m >> u) & 1) {
+                W[u] += T->thr[c];
+                stk[sp++] = c;
+            } else {
+                lm += T->thr[c];
+            }
+        }
+    }
+    return lm;
+}
+
+/*
+ * The relative L1 global-balance residual r(pi) of Eq. balance_eq_heter
+ * (reading C3) with O(2^(N - block_bits)) scratch: the rates
+ * of each state come from the prefix tree (ptree_rates), per-state terms are
+ * summed in ascending state order inside blocks of 2^block_bits states and the
+ * block sums in ascending block order.  num_out / den_out receive the two sums.
+ */
+double oracle_residual_stream(int N, int J, const double *lam, const double *mu, const int32_t *pref,
+                              const double *pi, int block_bits, double *num_out, double *den_out) {
+    inst_t I = {N, J, lam, mu, pref};
+    ptree_t T;
+    ptree_build(&I, &T);
+    if (block_bits > N) block_bits = N;
+    if (block_bits < 0) block_bits = 0;
+    const uint64_t nb = 1ULL << (N - block_bits), bs = 1ULL << block_bits;
+    double *bnum = (double *)malloc(sizeof(double) * nb), *bden = (double *)malloc(sizeof(double) * nb);
+    if (!bnum || !bden) { free(bnum); free(bden); ptree_free(&T); return NAN; }
+#pragma omp parallel
+    {
+        double W[64];
+        int *stk = (int *)malloc(sizeof(int) * (T.n + 1));
+#pragma omp for schedule(dynamic, 16)
+        for (int64_t b = 0; b < (int64_t)nb; b++) {
+            double sn = 0.0, sd = 0.0;
+            for (uint64_t k = 0; k < bs; k++) {
+                uint64_t m = ((uint64_t)b << block_bits) | k;
+                double lm = ptree_rates(&T, N, m, W, stk);
+                double out = pi[m] * (lm + mu_m(&I, m));
+                double in = 0.0;
+                for (int i = 0; i < N; i++) {
+                    uint64_t l = m ^ (1ULL << i);
+                    if ((m >> i) & 1) in += pi[l] * W[i];   /* upward transition into m   */
+                    else in += pi[l] * mu[i];                /* downward transition into m */
+                }
+                sn += fabs(out - in);
+                sd += out;
+            }
+            bnum[b] = sn;
+            bden[b] = sd;
+        }
+        free(stk);
+    }
+    double num = 0.0, den = 0.0;
+    for (uint64_t b = 0; b < nb; b++) { num += bnum[b]; den += bden[b]; }
+    free(bnum); free(bden); ptree_free(&T);
+    if (num_out) *num_out = num;
+    if (den_out) *den_out = den;
+    return num / den;
+}
+
+/* Eq. tran_rates through the prefix tree at one state (tests: equals
+ * oracle_dispatch_rates / lambda_m by list scans).  Returns lambda_m. */
+double oracle_tree_rates(int N, int J, const double *lam, const int32_t *pref, uint64_t m, double *W) {
+    inst_t I = {N, J, lam, NULL, pref};
+    ptree_t T;
+    ptree_build(&I, &T);
+    int *stk = (int *)malloc(sizeof(int) * (T.n + 1));
+    double lm = ptree_rates(&T, N, m, W, stk);
+    free(stk);
+    ptree_free(&T);
+    return lm;
+}
+
+double oracle_lambda_m(int N, int J, const double *lam, const int32_t *pref, uint64_t m) {
+    inst_t I = {N, J, lam, NULL, pref};
+    return lambda_m(&I, m);
 }
 
 /*

@@ -232,3 +232,86 @@ def test_alg1_residual_decreases_geometrically():
     ratios = tr[11:] / tr[10:-1]
     assert (ratios < 1.0).all()
     assert 0.3 < np.median(ratios) < 0.95
+
+
+# ---------------------------------------------------------------- iterate order (Algorithm 1)
+
+def test_first_sweep_hand_worked_n3():
+    """Algorithm 1's first sweep on a hand-worked N = 3 instance: one
+    atom with the list (0, 1, 2), lambda = 1, nu = (1, 2, 3).  Worked by hand from
+    Eq. updateHeter with the initial p_n = 1/C(3, n) and the initial
+    layer rates lambda(n) = 1 (n < 3), mu(1) = 2, mu(2) = 4, mu(3) = 6 (Eqs. lambdaHeter,
+    muHeter; reading C8):
+
+      layer 1 (k = 1): a = (1/2, 0, 0), b = (5/24, 1/9, 1/16) for m = 001, 010, 100
+        (b carries lambda(1)/mu(2) = 1/4); inner limit mu* = (89/144) / (1 - 1/2) = 89/72
+        -> p_1 = (119/144, 16/144, 9/144).
+      layer 2 (k = 1) reads the NEW p_1 (sequential order): for m = 011, 101, 110
+        A = (16/144 + 119/144, 9/144, 0), den = (4, 5, 6) -> a = (15/64, 1/80, 0);
+        D = (3, 2, 1), lambda(2)/mu(3) = 1/6 -> b = (1/8, 1/15, 1/36);
+        mu* = (281/360) / (1 - 241/320) = 2248/711.
+      pi after the sweep: Prop. 1 with Eq. bnd_stationary on lambda = (1, 1, 1, 0),
+        mu = (-, 89/72, 2248/711, 6).
+
+    An oracle that read the previous sweep's p_1 for layer 2 (Jacobi) gives
+    A(011) = 2/3 instead of 15/16 and fails this pin."""
+    from fractions import Fraction as F
+
+    inst = hqinst.from_arrays([1.0], [1.0, 2.0, 3.0], [[0, 1, 2]], name="N3-hand")
+    p1 = {0b001: F(119, 144), 0b010: F(16, 144), 0b100: F(9, 144)}
+    ms2 = F(2248, 711)
+    a2 = {0b011: F(15, 64), 0b101: F(1, 80), 0b110: F(0)}
+    b2 = {0b011: F(1, 8), 0b101: F(1, 15), 0b110: F(1, 36)}
+    p2 = {m: ms2 * a2[m] + b2[m] for m in a2}
+    assert sum(p2.values()) == 1 and sum(p1.values()) == 1
+    g = [F(1), F(72, 89)]
+    g.append(g[1] * 1 / ms2)
+    g.append(g[2] * 1 / 6)
+    tot = sum(g)
+    ref = np.zeros(8)
+    ref[0] = float(g[0] / tot)
+    ref[7] = float(g[3] / tot)
+    for m, v in p1.items():
+        ref[m] = float(g[1] / tot * v)
+    for m, v in p2.items():
+        ref[m] = float(g[2] / tot * v)
+    r = oracle.solve(inst, tol=0.0, max_iter=1)
+    assert r["iters"] == 1
+    np.testing.assert_allclose(r["pi"], ref, rtol=0, atol=2e-16)
+    np.testing.assert_allclose(r["layer_mu"][1:3], [89 / 72, 2248 / 711], rtol=1e-15)
+
+
+# ---------------------------------------------------------------- memory-lean residual
+
+@pytest.mark.parametrize("cfg,N,J", [(2, 12, 60), (4, 12, 60), (3, 14, 80), (5, 15, 200)])
+def test_tree_rates_match_list_scans(cfg, N, J):
+    """The prefix-tree rates of oracle_residual_stream equal Algorithm 3 by list scans
+    (dispatch_rates) and lambda_m by list scans, state by state (full and truncated lists)."""
+    inst = hqinst.config_instance(cfg, N=N, J=J)
+    rng = np.random.default_rng(N)
+    for m in rng.integers(0, 1 << N, 64):
+        W1 = oracle.dispatch_rates(inst, int(m))
+        W2, lm = oracle.tree_rates(inst, int(m))
+        scale = inst.lam.sum()
+        assert np.abs(W1 - W2).max() <= 1e-14 * scale
+        assert abs(lm - oracle.lambda_m(inst, int(m))) <= 1e-14 * scale
+
+
+@pytest.mark.parametrize("cfg,N,J", [(1, 10, 20), (2, 12, 60), (4, 12, 60), (3, 14, 80)])
+def test_residual_stream_matches_residual(cfg, N, J):
+    """oracle_residual_stream is the residual of Eq. balance_eq_heter (reading C3) evaluated
+    with block sums: equal to oracle_residual on arbitrary vectors (not only near a
+    solution) and at the solution, for every block size."""
+    inst = hqinst.config_instance(cfg, N=N, J=J)
+    rng = np.random.default_rng(3)
+    x = rng.random(1 << N)
+    x /= x.sum()
+    r1 = oracle.residual(inst, x)
+    for bb in (0, 5, N):
+        r2, num, den = oracle.residual_stream(inst, x, bb)
+        assert abs(r2 - r1) <= 1e-13 * r1
+        assert num > 0 and den > 0
+    sol = oracle.solve(inst, tol=1e-13)["pi"]
+    r1 = oracle.residual(inst, sol)
+    r2, _, _ = oracle.residual_stream(inst, sol, 6)
+    assert r2 <= 1e-13 and abs(r2 - r1) <= 1e-15
