@@ -1102,7 +1102,7 @@ static hq_status v3_prepare(hq_problem *h, cudaStream_t s) {
         bool chunked = N >= 27;
         if (om == "popcount") chunked = false;
         if (om == "chunk") chunked = true;
-        int b = 3;
+        int b = 5;   // measured: cfg4 b = 1 / 3 / 5 -> 2.71 / 2.64 / 2.41 s (popcount order 2.95 s)
         if (const char *benv = getenv("HQ_CHUNK_BITS")) b = atoi(benv);
         b = std::max(0, std::min(b, Nt));
         if (chunked && ((ntiles >> b) < (uint64_t)h->sgrid)) chunked = false;   // too few chunks to spread

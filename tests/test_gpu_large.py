@@ -126,15 +126,6 @@ def test_cfg4_truncated_n28(hq):
     assert g["loss"] > float(g["pi"][-1])
 
 
-def test_cfg5_n31(hq):
-    inst = hqinst.config_instance(5, rho=0.6)
-    g = solve(hq, inst)
-    pi = _large_checks(inst, g)
-    # layer-cut balance: pi(C_{n-1}) lambda = pi(C_n) mu(n) summed over the cut; here via
-    # the full-list identity sum_n<N masses = 1 - pi(all busy) and loss = pi(all busy)
-    assert abs(g["loss"] - float(pi[-1])) <= 1e-15
-
-
 def test_ordered_hunt_n31_closed_form(hq):
     N = 31
     order = np.random.default_rng(31).permutation(N).astype(np.int32)
