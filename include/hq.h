@@ -232,7 +232,9 @@ const char *hq_error_string(hq_handle h);
  *   [14] largest rate-program block of a CTA tile (16-byte records),
  *   [15] warp bits varying inside a rate program (0: one program per warp tile,
  *        the default; nW: one program per CTA tile, HQ_PROG=cta),
- *   [16], [17] reserved (0),
+ *   [16] device-resident solve: time of its one k_solve3 launch in ms (CUDA events),
+ *   [17] 1 if the solve ran device-resident (one launch for every half-sweep, check and
+ *        residual; [8] and [10] then split [16] by the phases' timestamps), 0 if host-looped,
  *   [18] tile visit order of the CTA-tiled path: -1 popcount order, b >= 0 chunked
  *        order with chunks of 2^b tiles (N >= 27).
  */

@@ -361,6 +361,9 @@ struct hq_problem {
     double q_last = 0.0;     // P~{C} (finite C), 0 for an unlimited buffer
     double stats[HQ_STATS_LEN] = {0};
     // device memory
+    bool dev_loop = true;          // path 3: device-resident solve (k_loop3); HQ_LOOP=host: one launch per half-sweep
+    Ctl3 *d_ctl = nullptr, *h_ctl = nullptr;   // path 3, device loop: control block (+ pinned mirror)
+    unsigned long long *d_xg = nullptr;        // path 3, device loop: exact phase sums
     int2 *d_node = nullptr;
     double *d_lthr = nullptr, *d_lend = nullptr;
     double *d_lam = nullptr;
@@ -383,7 +386,6 @@ struct hq_problem {
     bool chunked = false;          // path 3: chunked tile order (else popcount order)
     int chunk_bits = 0;            // path 3, chunked order: low tile bits per chunk
     std::vector<uint32_t> chunk_range;   // path 3, chunked order: CTA ranges over the visit order
-    float tune_ms[2] = {0.f, 0.f}; // path 3: timed sweeps with CTA / warp programs (0: not tuned)
     uint32_t *d_order = nullptr, *d_off16 = nullptr, *d_size16 = nullptr, *d_range = nullptr;
     uint4 *d_prog = nullptr;
     double2 *d_omkap = nullptr;
@@ -426,6 +428,11 @@ struct hq_problem {
         dfree(d_omkap);
         dfree(d_lamarr);
         dfree(d_blk);
+        dfree(d_ctl);
+        dfree(d_xg);
+        pinned_free(h_ctl, sizeof(Ctl3));
+        d_ctl = h_ctl = nullptr;
+        d_xg = nullptr;
         if (side) cudaStreamDestroy(side);
         if (ev_fork) cudaEventDestroy(ev_fork);
         if (ev_join) cudaEventDestroy(ev_join);
@@ -539,6 +546,10 @@ extern "C" hq_status hq_create(int N, int J, const double *lambda, const double 
         for (int u = 0; u < N; u++) h->nu_int[u] = mu[h->perm[u]];
     }
     h->v2 = N >= 8;
+    // device-resident solve by default where it is the faster path (measured, DESIGN.md §9:
+    // N = 18 14.3 vs 16.2 ms; N = 24 145 vs 123 ms); HQ_LOOP=device|host overrides
+    h->dev_loop = N < 21;
+    if (const char *lenv = getenv("HQ_LOOP")) h->dev_loop = std::string(lenv) != "host";
     *out = h.release();
     return HQ_OK;
 }
@@ -576,8 +587,10 @@ static hq_status alloc_device(hq_problem *h) {
     const size_t nn = h->trie.node.size();
     auto alloc = [&](void **p, size_t bytes) -> cudaError_t { return dmalloc(p, bytes ? bytes : 16); };
     if (h->path == 3) {
+        // host loop: a grid of CTAs in waves; device loop: one co-resident CTA per SM
         const uint64_t nt3 = 1ull << (N - 9 - h->nW);
-        h->sgrid = (int)std::min<uint64_t>(nt3, (uint64_t)h->nsm * hq3_launch::ctas_per_sm(h->nW));
+        const int per_sm = h->dev_loop ? 1 : hq3_launch::ctas_per_sm(h->nW);
+        h->sgrid = (int)std::min<uint64_t>(nt3, (uint64_t)h->nsm * per_sm);
     } else {
         h->sgrid = hq2_launch::sweep_grid(h->nsm);
     }
@@ -1106,7 +1119,12 @@ static hq_status v3_prepare(hq_problem *h, cudaStream_t s) {
         if (const char *benv = getenv("HQ_CHUNK_BITS")) b = atoi(benv);
         b = std::max(0, std::min(b, Nt));
         if (chunked && ((ntiles >> b) < (uint64_t)h->sgrid)) chunked = false;   // too few chunks to spread
-        if (chunked) {
+        if (om == "natural") {
+            // device-resident solve: tiles in natural order, handed out dynamically in units of
+            // consecutive tiles, so the CTAs in flight work on neighbouring tiles and the
+            // tile-unit neighbours at distance 2^h < L2 window stay L2-resident
+            for (uint64_t t = 0; t < ntiles; t++) order.push_back((uint32_t)t);
+        } else if (chunked) {
             h->chunk_bits = b;
             h->chunked = true;
             std::vector<uint32_t> low;
@@ -1241,6 +1259,7 @@ static S2Args base_s2(hq_problem *h) {
 struct SolveOut {
     int sweeps = 0, halfsweeps = 0, launches = 0, nres = 0;
     double updates = 0.0, sweep_ms = 0.0, resid_ms = 0.0, res = INFINITY;
+    double kernel_ms = -1.0;   // device loop: the one solve launch (sweep_ms from its phase stamps)
     bool converged = false;
 };
 
@@ -1419,6 +1438,124 @@ static hq_status solve_v2(hq_problem *h, double tol, int max_iter, double *pi, c
     return HQ_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Path 3, device-resident solve: init kernels, then ONE cooperative launch of k_loop3 runs
+// every half-sweep, the convergence checks (device-side decision on the fused |dp| proxy) and
+// the verification residual; the host synchronises once, at the end.
+// ---------------------------------------------------------------------------
+static hq_status solve_dev(hq_problem *h, double tol, int max_iter, double *pi, cudaStream_t s, SolveOut &o) {
+    hq_status st = v3_prepare(h, s);
+    if (st != HQ_OK) return st;
+    const int N = h->N;
+    const uint64_t half = 1ull << (N - 1);
+    const int G = h->sgrid;
+    double *hs = h->h_small;
+    if (!h->d_ctl) {
+        if (dmalloc((void **)&h->d_ctl, sizeof(Ctl3)) != cudaSuccess ||
+            dmalloc((void **)&h->d_xg, sizeof(unsigned long long) * HQ_XG_WORDS) != cudaSuccess ||
+            pinned_alloc((void **)&h->h_ctl, sizeof(Ctl3)) != cudaSuccess) {
+            cudaGetLastError();
+            h->err = "device memory for the solve control block could not be allocated";
+            return HQ_E_NOMEM;
+        }
+    }
+    // --- init (Algorithm 1 step 2): uniform p, its layer sums, the first scalar step
+    for (int n = 0; n < 32; n++) hs[S_MUSTAR + n] = n <= N ? 1.0 / binom(N, n) : 0.0;
+    HQ_CUDA(cudaMemcpyAsync(h->d_small + S_MUSTAR, hs + S_MUSTAR, sizeof(double) * 32, cudaMemcpyHostToDevice, s));
+    HQ_CUDA(cudaMemsetAsync(h->d_blk, 0, sizeof(double) * V2S_TOTAL, s));
+    KArgs k = base_args(h);
+    for (int c = 0; c < 2; c++) {
+        class_arrays(h, k, c);
+        k.partial = h->d_partial + (size_t)c * h->grid * HQ_NL * HQ_NV;
+        k.omkap = h->d_omkap + (c ? half : 0);
+        k.lamarr = h->d_lamarr ? h->d_lamarr + (c ? half : 0) : nullptr;
+        HQ_CUDA(hqk_launch::init_v2(k, h->grid, s));
+    }
+    HQ_CUDA(hq2_launch::scalars(N, h->full_lists, h->Lam, 0, 0, 0, 2 * h->grid, h->d_partial, h->d_blk, s));
+    HQ_CUDA(cudaMemsetAsync(h->d_ctl, 0, sizeof(Ctl3), s));
+    HQ_CUDA(cudaMemsetAsync(h->d_xg, 0, sizeof(unsigned long long) * HQ_XG_WORDS, s));
+    o.launches += 4;
+
+    S3Args a;
+    memset(&a, 0, sizeof(a));
+    a.N = N;
+    a.nW = h->nW;
+    a.ntiles = 1ull << (N - 9 - h->nW);
+    a.Lam = h->Lam;
+    for (int u = 0; u < 32; u++) a.nu[u] = u < N ? h->nu_int[u] : 0.0;
+    a.order = h->d_order;
+    a.off16 = h->d_off16;
+    a.prog = h->d_prog;
+    a.total16 = h->total16;
+    a.maxblk16 = h->maxrec;
+    a.range = h->d_range;
+    a.full_lists = h->full_lists ? 1 : 0;
+    a.warp_programs = (h->prog_nwv == 0) ? 1 : 0;
+    a.all_staged = h->maxblk_all <= h->maxrec ? 1 : 0;
+    a.partial = h->d_partial;
+    a.xg = h->d_xg;
+    // fixed-point range of the exact sums: every per-layer sum is below M = (Lambda + sum nu)
+    // x max(1, (Lambda + sum nu) / min(Lambda, nu_min)) (p <= 1 per layer; omega, kappa <= that
+    // ratio; den <= Lambda + sum nu); 2^8 headroom; resolution 2^(xe - 32 HQ_XL)
+    {
+        double snu = 0.0, numin = INFINITY;
+        for (int u = 0; u < N; u++) {
+            snu += h->nu_int[u];
+            numin = std::min(numin, h->nu_int[u]);
+        }
+        const double tot = h->Lam + snu;
+        const double M = tot * std::max(1.0, tot / std::min(h->Lam, numin));
+        a.xe = std::ilogb(M) + 1 + 8;
+    }
+    a.pw = h->d_pw;
+    a.omkap_all = h->d_omkap;
+    a.blk = h->d_blk;
+    a.ctl = h->d_ctl;
+    a.tol = tol;
+    a.max_iter = max_iter;
+    if (hq3_launch::loop_occupancy(a, a.full_lists) < 1) {
+        h->err = "the device-resident solve kernel does not fit an SM";
+        return HQ_E_CUDA;
+    }
+    cudaEvent_t e0 = h->event(0), e1 = h->event(1);
+    HQ_CUDA(cudaEventRecord(e0, s));
+    HQ_CUDA(hq3_launch::loop(a, a.full_lists, G, s));
+    HQ_CUDA(cudaEventRecord(e1, s));
+    o.launches += 1;
+    HQ_CUDA(cudaMemcpyAsync(h->h_ctl, h->d_ctl, sizeof(Ctl3), cudaMemcpyDeviceToHost, s));
+    HQ_CUDA(cudaMemcpyAsync(h->h_blk, h->d_blk, sizeof(double) * V2S_TOTAL, cudaMemcpyDeviceToHost, s));
+    HQ_CUDA(hq2_launch::assemble(N, h->d_pw, h->d_blk + V2S_PN, h->perm.data(), pi, h->nsm * 8, s));
+    o.launches += 1;
+    HQ_CUDA(cudaStreamSynchronize(s));
+    float kms = 0.f;
+    cudaEventElapsedTime(&kms, e0, e1);
+    const Ctl3 &c = *h->h_ctl;
+    o.sweeps = c.sweeps;
+    o.halfsweeps = c.halfsweeps;
+    o.updates = c.updates;
+    o.nres = c.nres;
+    o.res = c.res;
+    o.converged = c.status == SOLVE3_CONVERGED;
+    // time split of the one launch by the globaltimer stamps of CTA 0 (sweep vs residual phases)
+    const double tot_ns = (double)c.ns_sweep + (double)c.ns_res;
+    o.sweep_ms = tot_ns > 0 ? kms * (double)c.ns_sweep / tot_ns : kms;
+    o.resid_ms = tot_ns > 0 ? kms * (double)c.ns_res / tot_ns : 0.0;
+    o.kernel_ms = kms;
+    for (int n = 0; n <= N; n++) hs[S_PN + n] = h->h_blk[V2S_PN + n + 1];
+    if (getenv("HQ_DEBUG_CTL"))
+        fprintf(stderr, "k_loop3: status %d sweeps %d halfsweeps %d nres %d phases %d res %.3e proxy %.3e grid %d\n",
+                c.status, c.sweeps, c.halfsweeps, c.nres, c.phases, c.res, c.proxy, G);
+    if (c.status == SOLVE3_NUMERIC) {
+        h->err = c.err ? "non-finite or out-of-range per-layer sum" : "non-positive or non-finite layer normaliser";
+        return HQ_E_NUMERIC;
+    }
+    if (c.status == SOLVE3_NOTDECR) {
+        h->err = "the residual proxy grew at four consecutive convergence checks (iteration diverges)";
+        return HQ_E_NUMERIC;
+    }
+    return HQ_OK;
+}
+
 static hq_status solve_core(hq_handle h, double tol, int max_iter, double *pi, void *cuda_stream, int *iters_out,
                             double *residual_out) {
     if (!h) return HQ_E_INVAL;
@@ -1442,7 +1579,7 @@ static hq_status solve_core(hq_handle h, double tol, int max_iter, double *pi, v
         HQ_CUDA(cudaEventCreate(&a1));
         HQ_CUDA(cudaEventRecord(a0, s));
         SolveOut o;
-        st = solve_v2(h, tol, max_iter, pi, s, o);
+        st = (h->path == 3 && h->dev_loop) ? solve_dev(h, tol, max_iter, pi, s, o) : solve_v2(h, tol, max_iter, pi, s, o);
         if (st != HQ_OK) {
             cudaEventDestroy(a0);
             cudaEventDestroy(a1);
@@ -1455,10 +1592,14 @@ static hq_status solve_core(hq_handle h, double tol, int max_iter, double *pi, v
         cudaEventDestroy(a0);
         cudaEventDestroy(a1);
         double sweep_ms = 0.0;
-        for (int i = 0; i < o.halfsweeps; i++) {
-            float x = 0.f;
-            cudaEventElapsedTime(&x, h->ev[2 * i], h->ev[2 * i + 1]);
-            sweep_ms += x;
+        if (o.kernel_ms >= 0.0) {
+            sweep_ms = o.sweep_ms;
+        } else {
+            for (int i = 0; i < o.halfsweeps; i++) {
+                float x = 0.f;
+                cudaEventElapsedTime(&x, h->ev[2 * i], h->ev[2 * i + 1]);
+                sweep_ms += x;
+            }
         }
         double sp = 0.0;
         for (int n = 0; n <= N; n++) sp += hs[S_PN + n];
@@ -1479,8 +1620,8 @@ static hq_status solve_core(hq_handle h, double tol, int max_iter, double *pi, v
         h->stats[13] = h->path;   // path id
         h->stats[14] = h->maxblk_all;
         h->stats[15] = h->prog_nwv;
-        h->stats[16] = h->tune_ms[0];
-        h->stats[17] = h->tune_ms[1];
+        h->stats[16] = o.kernel_ms >= 0.0 ? o.kernel_ms : 0.0;
+        h->stats[17] = o.kernel_ms >= 0.0 ? 1.0 : 0.0;
         h->stats[18] = h->chunked ? h->chunk_bits : -1;
         if (iters_out) *iters_out = o.sweeps;
         if (residual_out) *residual_out = o.res;

@@ -54,6 +54,42 @@ __device__ __forceinline__ void reduce_partials_t(const double *partial, int G, 
     }
 }
 
+// The same reduction read through L2 (k_loop3: the partials were written by other CTAs in
+// the same kernel, an SM may hold stale L1 lines of the buffer from two phases earlier).
+__device__ __forceinline__ void reduce_partials_t_cg(const double *partial, int G, int N, double (*S)[NV2], int lg,
+                                                  uint32_t only = 0u) {
+    int lay[HQ_NL];   // the reduced layers, ascending
+    int nl = 0;
+    for (int L = 0; L <= N; L++)
+        if (!only || ((only >> L) & 1u)) lay[nl++] = L;
+    const int items = nl * NV2;
+    const int tpi = 1 << lg, q = threadIdx.x & (tpi - 1);
+    // items rounded up to whole warps: every warp visits its items together, so the
+    // shuffles below are warp-uniform (blockDim.x is a multiple of 32)
+    const int per_warp = 32 >> lg;
+    const int nit = (items + per_warp - 1) / per_warp * per_warp;
+    for (int it = threadIdx.x >> lg; it < nit; it += blockDim.x >> lg) {
+        const int li = it / NV2, v = it - li * NV2;
+        const bool ok = li < nl;
+        const int L = ok ? lay[li] : 0;
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        if (ok) {
+            const double *src = partial + ((size_t)L * HQ_NV + v) * G;
+            int b = q;
+            for (; b + 3 * tpi < G; b += 4 * tpi) {
+                s0 += __ldcg(src + b);
+                s1 += __ldcg(src + b + tpi);
+                s2 += __ldcg(src + b + 2 * tpi);
+                s3 += __ldcg(src + b + 3 * tpi);
+            }
+            for (; b < G; b += tpi) s0 += __ldcg(src + b);
+        }
+        double s = (s0 + s1) + (s2 + s3);
+        for (int o = 1; o < tpi; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (q == 0 && ok) S[L][v] = s;
+    }
+}
+
 __device__ __forceinline__ void scalars_update(int N, int full_lists, double Lam, int mode, int c, uint32_t active,
                                                const double (*S)[NV2], double *sb) {
     double *lam = sb + V2S_LAM, *mu = sb + V2S_MU, *al = sb + V2S_ALPHA, *be = sb + V2S_BETA;

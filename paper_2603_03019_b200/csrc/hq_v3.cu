@@ -33,6 +33,7 @@
 // butterflies keyed by layer when popcount(tile) changes, a fixed-order sum
 // over the warps of the CTA, and k_scalars2's fixed-order sum over CTAs.
 #include <cuda_runtime.h>
+#include <cooperative_groups.h>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -43,6 +44,7 @@
 #include "hq_scalars.cuh"
 
 namespace hq3 {
+namespace cg = cooperative_groups;
 
 constexpr int R = V3_R;
 
@@ -197,12 +199,22 @@ __device__ __forceinline__ double unit_rates(const Prog<WP> &P, const uint4 &h, 
                                              const double (&q)[R], double (&A)[R]) {
     const uint32_t inf = h.x;
     if (!inf) return w0;
-    const uint4 *d = P.pg + V3_HDR16 + ((inf >> 8) & 0xffffu);
+    const uint4 *d = P.pg + V3_HDR16 + ((inf >> 8) & 0x3fffffu);
     double Wt = w0;
     if (inf >> 31) {
         const uint32_t Mt = h.y;
         Wt = reinterpret_cast<const double *>(d)[P.idx(Mt)];
         d += ((1 << __popc(Mt)) + 1) >> 1;
+    }
+    if ((inf >> 30) & 1u) {   // register table: summed rate per register state (this beta)
+        const double2 *wr = reinterpret_cast<const double2 *>(d) + (sh ? 4 : 0);
+#pragma unroll
+        for (int kk = 0; kk < 4; kk++) {
+            const double2 w = wr[kk];
+            A[2 * kk] = fma(w.x, q[2 * kk], A[2 * kk]);
+            A[2 * kk + 1] = fma(w.y, q[2 * kk + 1], A[2 * kk + 1]);
+        }
+        d += 8;
     }
     const int ng = (int)(inf & 0xffu);
     for (int g = 0; g < ng; g++) {
@@ -249,6 +261,95 @@ __device__ __forceinline__ double2 ldg_ef(const double2 *p) {
 
 
 
+
+// ---------------------------------------------------------------------------
+// Per-CTA context of the tiled sweep: shared-memory carve-up and per-thread constants,
+// set up once per kernel (k_sweep3: one half-sweep; k_solve3: the whole solve).
+// ---------------------------------------------------------------------------
+// shared memory of the tiled kernels (namespace scope: one copy per CTA of a kernel that uses it)
+extern __shared__ __align__(128) unsigned char smem3[];   // [2][q block | program block] | bins | flush
+__shared__ __align__(8) uint64_t tbar3[2];                 // mbarriers of the two tile buffers
+__shared__ double s_x3[32], s_y3[32], s_z3[32], s_mr3[R];  // phase coefficients per layer; mu of register states
+__shared__ uint8_t s_pext3[32 * 32];                       // [M5][lane] = pext(lane, M5)
+__shared__ uint8_t s_pextw3[16 * 16];                      // [M4][warp] = pext(warp, M4)
+
+// shared memory of the tiled kernels: dynamic [tile buffers | bins | flush scratch | extra],
+// static pext tables, coefficients, mbarriers (declared by the kernels)
+__device__ __forceinline__ void cta3_setup(const S3Args &a) {
+    const int tid = threadIdx.x;
+    if (tid < R)
+        s_mr3[tid] = ((tid & 1) ? a.nu[1] : 0.0) + ((tid & 2) ? a.nu[7] : 0.0) + ((tid & 4) ? a.nu[8] : 0.0);
+    for (int i = tid; i < 32 * 32; i += blockDim.x) {   // pext of lane bits: s_pext[M * 32 + l]
+        const uint32_t M = (uint32_t)i >> 5, l = (uint32_t)i & 31u;
+        uint32_t r = 0;
+        for (int b = 0, j = 0; b < 5; b++)
+            if ((M >> b) & 1u) r |= ((l >> b) & 1u) << j++;
+        s_pext3[i] = (uint8_t)r;
+    }
+    for (int i = tid; i < 16 * 16; i += blockDim.x) {
+        const uint32_t M = (uint32_t)i >> 4, w = (uint32_t)i & 15u;
+        uint32_t r = 0;
+        for (int b = 0, j = 0; b < 4; b++)
+            if ((M >> b) & 1u) r |= ((w >> b) & 1u) << j++;
+        s_pextw3[i] = (uint8_t)r;
+    }
+}
+
+// nu summed over the busy lane and warp units of this thread (tile units: mu_F of the program)
+__device__ __forceinline__ double thread_mu3(const S3Args &a) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double mu_t = 0.0;
+#pragma unroll
+    for (int b = 0; b < 5; b++)
+        if ((lane >> b) & 1) mu_t += a.nu[2 + b];
+    for (int b = 0; b < a.nW; b++)
+        if ((warp >> b) & 1) mu_t += a.nu[9 + b];
+    return mu_t;
+}
+
+// thread 0: issue the bulk copies of tile k of the range [i0, ..) (read class Q) into buffer g & 1
+// (q block of the tile in the read class + its program block if it fits the staging area)
+__device__ __forceinline__ void load_tile3(const S3Args &a, const double *Q, uint32_t i0, int k, uint32_t g) {
+    const int nW = a.nW, T = 8 + nW;
+    const uint32_t TS = 1u << T, nwarps = 1u << nW;
+    const size_t BUFD = TS + 2 * (size_t)a.maxblk16;
+    const uint64_t nwt = (uint64_t)a.ntiles << nW;   // per-warp program slots
+    const uint64_t widx = (uint64_t)(i0 + k) << nW;
+    const uint32_t t = __ldg(a.order + (i0 + k));
+    const uint32_t o = __ldg(a.off16 + widx);
+    const uint32_t nrec = (widx + nwarps < nwt ? __ldg(a.off16 + widx + nwarps) : a.total16) - o;
+    const bool staged = nrec <= a.maxblk16;
+    const int buf = g & 1;
+    const unsigned bar = sptr(&tbar3[buf]);
+    double *b = reinterpret_cast<double *>(smem3) + (size_t)buf * BUFD;
+    mbar_expect(bar, TS * 8u + (staged ? nrec * 16u : 0u));
+#ifndef HQ_NO_L2POL
+    bulk_g2s_pol(sptr(b), Q + ((size_t)t << T), TS * 8u, bar, pol_evict_last());
+    if (staged) bulk_g2s_pol(sptr(b + TS), a.prog + o, nrec * 16u, bar, pol_evict_first());
+#else
+    bulk_g2s(sptr(b), Q + ((size_t)t << T), TS * 8u, bar);
+    if (staged) bulk_g2s(sptr(b + TS), a.prog + o, nrec * 16u, bar);
+#endif
+}
+
+// coefficients of a phase: MODE 0/1 alpha(n), beta(n) of the half-sweep; MODE 2 the layer
+// masses p(n) (index n + 1 of V2S_PN).  coef: the scalar block (global or shared).
+template <int MODE>
+__device__ __forceinline__ void load_coef3(const double *coef) {
+    const int tid = threadIdx.x;
+    if (tid < 32) {
+        if (MODE == 2) {
+            const double *pn1 = coef + V2S_PN;   // pn1[n + 1] = p(n)
+            s_x3[tid] = pn1[tid];
+            s_y3[tid] = tid + 2 < 34 ? pn1[tid + 2] : 0.0;
+            s_z3[tid] = pn1[tid + 1];
+        } else {
+            s_x3[tid] = coef[V2S_ALPHA + tid];
+            s_y3[tid] = coef[V2S_BETA + tid];
+            s_z3[tid] = 0.0;
+        }
+    }
+}
 
 // ST: every program block is staged (host-checked S3Args::all_staged): program reads are
 // plain shared-memory loads with 32-bit addressing
@@ -703,6 +804,730 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
     }
 }
 
+
+// ===========================================================================
+// Device-resident solve (k_loop3): ONE cooperative launch runs Algorithm 1's
+// whole sweep loop (red-black staggered schedule), the
+// convergence checks and the verification residual.  It is the sweep kernel's tile loop
+// (k_sweep3: static contiguous tile ranges, fixed-order per-CTA sums) inside a phase loop:
+//   phase = one half-sweep of class t & 1 (mode 0, or mode 1 with the |dp| sums of a check),
+//           or the verification residual over both classes (mode 2);
+//   after a grid barrier every CTA performs the same scalar step (hq_scalars.cuh, the fixed-
+//   order reduction of the CTA partials) on its shared-memory copy of the scalar block and
+//   takes the same control decision (check schedule, residual trigger, stop).  The host
+//   synchronises once, when the kernel has stopped.
+// The phase parameters live in shared memory and are read `volatile` where the tile loop
+// needs them, so that they do not occupy registers across the loop.
+// ===========================================================================
+struct Loop3Smem {
+    // phase (thread 0 writes them before a barrier)
+    int c, mode;                 // class updated / evaluated; 0 sweep, 1 sweep + |dp|, 2 residual
+    uint32_t active;             // layers updated (sweep)
+    const double *Q;             // read class
+    double *P;                   // written (sweep) / evaluated (residual) class
+    const double2 *omk;          // scatter weights of class c
+    // control (identical in every CTA)
+    int kind, t, next_check, prev_check, rise, status, sweeps, halfsweeps, nres, phases, pbuf;
+    double updates, prev_proxy, proxy, res, rate, dprev;
+    unsigned long long tp0, ns_sweep, ns_res;
+};
+__shared__ Loop3Smem L3;
+enum { K3_SWEEP = 0, K3_RESID = 1, K3_FINAL = 2, K3_DONE = 3 };
+
+template <class T>
+__device__ __forceinline__ T vld(const T &x) { return *(const volatile T *)&x; }
+
+// Exact (order-independent) phase sums: every per-layer sum is >= 0 and is accumulated in
+// fixed point, HQ_XL 32-bit limbs held in 64-bit words (carries collect in the high halves),
+// unit 2^(xe - 32 HQ_XL); integer addition is associative, so the CTAs' atomics give the
+// same bits in any order (bitwise reproducible), and no CTA has to reduce the others' partials.
+__device__ __forceinline__ bool xadd_g(unsigned long long *xa, double x, int xe) {
+    if (x == 0.0) return true;
+    if (!(x > 0.0) || isinf(x)) return false;
+    const unsigned long long bits = (unsigned long long)__double_as_longlong(x);
+    int ex = (int)(bits >> 52);
+    unsigned long long m = bits & ((1ull << 52) - 1);
+    if (ex == 0) ex = 1;
+    else m |= 1ull << 52;
+    const int s = ex - 1075 - xe + 32 * HQ_XL;   // x = m 2^(ex-1075) = (m << s) units
+    if (s + 53 > 32 * HQ_XL) return false;
+#pragma unroll
+    for (int k = 0; k < HQ_XL; k++) {
+        const int d = s - 32 * k;
+        unsigned long long v;
+        if (d >= 0) v = d < 64 ? (m << d) : 0ull;
+        else v = -d < 64 ? (m >> -d) : 0ull;
+        v &= 0xffffffffull;
+        if (v) atomicAdd(xa + k, v);
+    }
+    return true;
+}
+// value of an accumulator (read through L2: other CTAs' atomics), limbs summed from the top
+__device__ __forceinline__ double xget(const unsigned long long *xa, int xe) {
+    uint32_t limb[HQ_XL + 1];
+    unsigned long long carry = 0;
+#pragma unroll
+    for (int k = 0; k < HQ_XL; k++) {
+        const unsigned long long v = __ldcg(xa + k) + carry;
+        limb[k] = (uint32_t)v;
+        carry = v >> 32;
+    }
+    limb[HQ_XL] = (uint32_t)carry;
+    double d = 0.0;
+#pragma unroll
+    for (int k = HQ_XL; k >= 0; k--) d = d * 4294967296.0 + (double)limb[k];
+    return ldexp(d, xe - 32 * HQ_XL);
+}
+
+
+// 16-byte load through L2 with a cache policy (k_loop3: the read class was written by other
+// CTAs earlier in the same kernel, so no L1 / non-coherent path)
+__device__ __forceinline__ double2 ldg2cg(const double *p, uint64_t pol) {
+    double2 v;
+    asm volatile("ld.global.cg.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+    return v;
+}
+
+// neighbour-slice load of k_loop3: HQ_LOOP_CG builds read through L2 (.cg); the default is the
+// read-only path without L1 allocation, safe here because no load of the class arrays in this
+// kernel allocates L1 lines (bulk copies go to shared memory, the old p is read .cg), so every
+// such load is served by L2, which the grid barrier makes coherent
+__device__ __forceinline__ double2 ldg2nc_loop(const double *p, uint64_t pol) {
+#ifdef HQ_LOOP_CG
+    return ldg2cg(p, pol);
+#else
+    return ldg2(p, pol);
+#endif
+}
+
+// layers updated by half-sweep t of the staggered schedule (host solve_v2 uses the same rule)
+__device__ __forceinline__ uint32_t active_mask3(int t, int N, int max_iter) {
+    uint32_t act = 0;
+    for (int n = 1; n <= N - 1; n++)
+        if (((t - n) & 1) == 0 && n <= t && (t - n) / 2 < max_iter) act |= 1u << n;
+    return act;
+}
+
+// thread 0: parameters of the next phase from the control state (pass: residual class)
+__device__ __forceinline__ void loop3_phase(const S3Args &a, int pass) {
+    const size_t half = (size_t)1 << (a.N - 1);
+    const int kind = L3.kind;
+    if (kind == K3_SWEEP) {
+        L3.c = L3.t & 1;
+        L3.active = active_mask3(L3.t, a.N, a.max_iter);
+        L3.mode = (a.tol > 0.0 && L3.t >= L3.next_check - 1) ? 1 : 0;
+    } else {
+        L3.c = pass;
+        L3.active = 0u;
+        L3.mode = 2;
+    }
+    const int c = L3.c;
+    L3.Q = a.pw + (c ? 0 : half);
+    L3.P = a.pw + (c ? half : 0);
+    L3.omk = a.omkap_all + (c ? half : 0);
+}
+
+// control decision after a phase (thread 0; identical in every CTA)
+__device__ void loop3_control(const S3Args &a, const double *blk, double num, double den, int gerr) {
+    const int N = a.N, kind = L3.kind, t = L3.t, mode = L3.mode;
+    const uint32_t active = L3.active;
+    L3.phases++;
+    int next = K3_SWEEP;
+    if (kind == K3_SWEEP) {
+        L3.halfsweeps++;
+        double bn = 1.0;   // C(N, n), exact in fp64 for N <= 31
+        for (int n = 1; n <= N - 1; n++) {
+            bn = bn * (double)(N - n + 1) / (double)n;
+            if ((active >> n) & 1u) L3.updates += floor(bn + 0.5);
+        }
+        if ((active >> (N - 1)) & 1u) L3.sweeps = (t - (N - 1)) / 2 + 1;
+        if (gerr || blk[V2S_MISC + 0] != 0.0) {
+            L3.status = SOLVE3_NUMERIC;
+            next = K3_DONE;
+        } else if (mode == 1 && t >= L3.next_check) {
+            const double proxy = blk[V2S_MISC + 2];
+            L3.proxy = proxy;
+            if (!isfinite(proxy)) {
+                L3.status = SOLVE3_NUMERIC;
+                next = K3_DONE;
+            } else {
+                double rate = 0.0;
+                if (L3.prev_proxy > 0.0 && t > L3.prev_check)
+                    rate = pow(proxy / L3.prev_proxy, 1.0 / (double)(t - L3.prev_check));
+                L3.rate = rate;
+                // a residual proxy that grows by > 1.5x at four consecutive checks: the
+                // iteration diverges (Assumption 1, does not hold)
+                L3.rise = (L3.prev_proxy > 0.0 && proxy > 1.5 * L3.prev_proxy) ? L3.rise + 1 : 0;
+                L3.prev_proxy = proxy;
+                L3.prev_check = t;
+                if (L3.rise >= 4) {
+                    L3.status = SOLVE3_NOTDECR;
+                    next = K3_DONE;
+                } else if (proxy <= 2.0 * a.tol) {
+                    next = K3_RESID;
+                } else {
+                    int gap = 24;
+                    if (rate > 0.0 && rate < 0.999)
+                        gap = min(200, max(2, (int)floor(0.9 * log(a.tol / proxy) / log(rate))));
+                    L3.next_check = t + gap;
+                }
+            }
+        }
+        L3.t = t + 1;
+        if (next == K3_SWEEP && !active_mask3(t + 1, N, a.max_iter)) next = K3_FINAL;
+    } else {
+        L3.res = num / den;
+        L3.nres++;
+        if (gerr || !isfinite(L3.res)) {
+            L3.status = SOLVE3_NUMERIC;
+            next = K3_DONE;
+        } else if (a.tol > 0.0 && L3.res <= a.tol) {
+            L3.status = SOLVE3_CONVERGED;
+            next = K3_DONE;
+        } else if (kind == K3_FINAL) {
+            L3.status = SOLVE3_MAXITER;
+            next = K3_DONE;
+        } else {
+            int gap = 24;
+            const double rate = L3.rate;
+            if (rate > 0.0 && rate < 0.999)
+                gap = min(200, max(2, (int)floor(0.9 * log(a.tol / L3.res) / log(rate))));
+            L3.next_check = L3.prev_check + gap;
+            next = active_mask3(L3.t, N, a.max_iter) ? K3_SWEEP : K3_FINAL;
+        }
+    }
+    L3.kind = next;
+}
+
+template <bool FULL, bool WP, bool ST>
+__global__ void __launch_bounds__(512, 1) k_loop3(const __grid_constant__ S3Args a) {
+    using SL = Slots<0, FULL>;   // per-layer bins of a sweep (residual phases use two of them)
+    constexpr int NB = SL::NB;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    __shared__ __align__(8) uint64_t tbar[2];
+    __shared__ double s_x[32], s_y[32], s_z[32], s_mr[R], s_w[32];
+    __shared__ double s_red[16];
+    __shared__ uint8_t s_pext[32 * 32];   // [M5][lane] = pext(lane, M5)
+    __shared__ uint8_t s_pextw[16 * 16];  // [M4][warp] = pext(warp, M4)
+    cg::grid_group grid = cg::this_grid();
+
+    const int nW = a.nW, T = 8 + nW, NVU = 9 + nW, nH = a.N - NVU;
+    const int tid = threadIdx.x, lane = tid & 31, warp = wuni(tid >> 5);
+    const unsigned nwarps = 1u << nW;
+    const uint32_t TS = 1u << T;
+    // smem: tile buffers [2][q block | program block], per-thread bins [3 * 5][threads],
+    //       per-warp flush scratch [warps][32 * 3], this CTA's scalar block, phase sums
+    const size_t BUFD = TS + 2 * (size_t)a.maxblk16;
+    double *tileq = reinterpret_cast<double *>(smem_raw);
+    double *sb = tileq + 2 * BUFD;
+    const int nthr = 32 << nW;
+    double *fscr = sb + (size_t)3 * 5 * nthr + (size_t)warp * 32 * 3;
+    double *s_blk = sb + (size_t)3 * 5 * nthr + (size_t)nwarps * 32 * 3;
+    double(*s_S)[NV2] = reinterpret_cast<double(*)[NV2]>(s_blk + V2S_TOTAL);
+
+    const uint32_t i0 = __ldg(a.range + blockIdx.x), i1 = __ldg(a.range + blockIdx.x + 1);
+    const int nt = (int)(i1 - i0);
+    const uint64_t nwt = (uint64_t)a.ntiles << nW;   // per-warp program slots
+    auto load_tile = [&](int k, uint32_t gk) {       // thread 0: tile k of the range into buffer gk & 1
+        const uint64_t widx = (uint64_t)(i0 + k) << nW;
+        const uint32_t tt = __ldg(a.order + (i0 + k));
+        const uint32_t o = __ldg(a.off16 + widx);
+        const uint32_t nrec = (widx + nwarps < nwt ? __ldg(a.off16 + widx + nwarps) : a.total16) - o;
+        const bool staged = nrec <= a.maxblk16;
+        const int buf = gk & 1;
+        const unsigned bar = sptr(&tbar[buf]);
+        double *b = tileq + (size_t)buf * BUFD;
+        mbar_expect(bar, TS * 8u + (staged ? nrec * 16u : 0u));
+        bulk_g2s_pol(sptr(b), vld(L3.Q) + ((size_t)tt << T), TS * 8u, bar, pol_evict_last());
+        if (staged) bulk_g2s_pol(sptr(b + TS), a.prog + o, nrec * 16u, bar, pol_evict_first());
+    };
+    // ---- once: barriers, tables, the scalar block, the control state
+    if (tid == 0) {
+        mbar_init(sptr(&tbar[0]), 1);
+        mbar_init(sptr(&tbar[1]), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        L3.t = 1;
+        L3.next_check = a.N + 2 * 12;
+        L3.prev_check = 0;
+        L3.prev_proxy = -1.0;
+        L3.proxy = 0.0;
+        L3.rate = 0.0;
+        L3.rise = 0;
+        L3.res = INFINITY;
+        L3.status = SOLVE3_RUNNING;
+        L3.sweeps = L3.halfsweeps = L3.nres = L3.phases = 0;
+        L3.updates = 0.0;
+        L3.pbuf = 0;
+        L3.dprev = 0.0;
+        L3.ns_sweep = L3.ns_res = 0ull;
+        L3.kind = active_mask3(1, a.N, a.max_iter) ? K3_SWEEP : K3_FINAL;
+    }
+    for (int i = tid; i < V2S_TOTAL; i += blockDim.x) s_blk[i] = a.blk[i];
+    if (tid < R)
+        s_mr[tid] = ((tid & 1) ? a.nu[1] : 0.0) + ((tid & 2) ? a.nu[7] : 0.0) + ((tid & 4) ? a.nu[8] : 0.0);
+    for (int i = tid; i < 32 * 32; i += blockDim.x) {   // pext of lane bits: s_pext[M * 32 + l]
+        const uint32_t M = (uint32_t)i >> 5, l = (uint32_t)i & 31u;
+        uint32_t r = 0;
+        for (int b = 0, j = 0; b < 5; b++)
+            if ((M >> b) & 1u) r |= ((l >> b) & 1u) << j++;
+        s_pext[i] = (uint8_t)r;
+    }
+    for (int i = tid; i < 16 * 16; i += blockDim.x) {
+        const uint32_t M = (uint32_t)i >> 4, w = (uint32_t)i & 15u;
+        uint32_t r = 0;
+        for (int b = 0, j = 0; b < 4; b++)
+            if ((M >> b) & 1u) r |= ((w >> b) & 1u) << j++;
+        s_pextw[i] = (uint8_t)r;
+    }
+    // ---- per-thread constants
+    double mu_t = 0.0;   // busy lane and warp units of this thread (tile units: mu_F of the program)
+#pragma unroll
+    for (int b = 0; b < 5; b++)
+        if ((lane >> b) & 1) mu_t += a.nu[2 + b];
+    for (int b = 0; b < nW; b++)
+        if ((warp >> b) & 1) mu_t += a.nu[9 + b];
+    const int popc_t = __popc(lane) + __popc(warp);
+    const int par_t = popc_t & 1;
+    const uint32_t jw = ((uint32_t)warp << 8) | ((uint32_t)lane << 1);   // j_local(r) = jw | (r>>1)<<6 | (r&1)
+    const double nu0 = a.nu[0];
+    const uint64_t pol_ef = pol_evict_first(), pol_el = pol_evict_last();
+    uint32_t g = 0;   // tiles this CTA has processed (tile-buffer mbarrier phases)
+
+    for (;;) {
+        __syncthreads();   // control state of the previous phase visible
+        if (L3.kind == K3_DONE) break;
+        const int npass = L3.kind == K3_SWEEP ? 1 : 2;
+        if (tid == 0 && blockIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(L3.tp0));
+        for (int pass = 0; pass < npass; pass++) {
+            if (tid == 0) {
+                loop3_phase(a, pass);
+                if (nt > 0) {
+                    fence_proxy_async();   // the buffer was read by the generic proxy before
+                    load_tile(0, g);
+                }
+            }
+            __syncthreads();
+            if (tid < 32) {   // phase coefficients (s_w: layer masses p(n), weights of the check)
+                s_w[tid] = s_blk[V2S_PN + tid + 1];
+                if (L3.mode == 2) {
+                    const double *pn1 = s_blk + V2S_PN;   // pn1[n + 1] = p(n)
+                    s_x[tid] = pn1[tid];
+                    s_y[tid] = tid + 2 < 34 ? pn1[tid + 2] : 0.0;
+                    s_z[tid] = pn1[tid + 1];
+                } else {
+                    s_x[tid] = s_blk[V2S_ALPHA + tid];
+                    s_y[tid] = s_blk[V2S_BETA + tid];
+                    s_z[tid] = 0.0;
+                }
+            }
+            double acc[NB];   // lane L: layer L
+#pragma unroll
+            for (int v = 0; v < NB; v++) acc[v] = 0.0;
+            double dsum = 0.0;   // check phases: sum of p(n) |p_new - p_old| over this thread's states
+#pragma unroll
+            for (int h = 0; h < 3; h++)
+#pragma unroll
+                for (int v = 0; v < NB; v++) sb[(h * NB + v) * nthr + tid] = 0.0;
+            int curK = -1;
+            // layer of bin h of this thread at tile popcount K: K + popc_t + beta + 2h.
+            auto flush = [&]() {
+                if (curK < 0) return;
+                const int cc = vld(L3.c);
+                const int betaK = cc ^ (curK & 1) ^ par_t;
+                const int p0 = (cc ^ curK ^ __popc(warp)) & 1;
+                const int L0 = curK + __popc(warp) + p0;                   // lowest layer of the warp
+                const int z = (popc_t - __popc(warp) + betaK - p0) >> 1;   // this lane's bins sit at L0 + 2 (z + h)
+                const int y = lane;                                        // lanes 0..5: relative layer L0 + 2y
+#pragma unroll
+                for (int v = 0; v < NB; v++) {
+#pragma unroll
+                    for (int h = 0; h < 3; h++) fscr[lane * 3 + h] = sb[(h * NB + v) * nthr + tid];
+                    __syncwarp();
+                    double s = 0.0;
+                    for (int l = 0; l < 32; l++) {   // fixed lane order
+                        const int hh = y - __shfl_sync(0xffffffffu, z, l);
+                        if (y < 6 && hh >= 0 && hh < 3) s += fscr[l * 3 + hh];
+                    }
+                    __syncwarp();
+#pragma unroll
+                    for (int yy = 0; yy < 6; yy++) {
+                        const double x = __shfl_sync(0xffffffffu, s, yy);
+                        if (lane == L0 + 2 * yy) acc[v] += x;
+                    }
+                }
+#pragma unroll
+                for (int h = 0; h < 3; h++)
+#pragma unroll
+                    for (int v = 0; v < NB; v++) sb[(h * NB + v) * nthr + tid] = 0.0;
+            };
+            __syncthreads();   // coefficients written
+            for (int k = 0; k < nt; k++) {
+                const uint32_t tidx = i0 + k;
+                const uint32_t t = __ldg(a.order + tidx);
+                const uint32_t jt = t << T;
+                const uint32_t gk = g + (uint32_t)k;
+                const int buf = gk & 1;
+                // tile-unit neighbour slices: two units of loads in flight ahead of the one accumulated
+                // class arrays of this phase: offsets of the parameter bases by the class (read
+                // once per tile from shared memory)
+                const int cph = vld(L3.c);
+                const size_t coff = (size_t)cph << (a.N - 1);
+                const double *Qt = a.pw + (((size_t)1 << (a.N - 1)) - coff);
+                auto hsrc = [&](int h) -> const double * { return Qt + ((jt ^ (1u << (T + h))) | jw); };
+                double2 pa[4], pb2[4];
+                if (nH > 0) {
+#pragma unroll
+                    for (int kk = 0; kk < 4; kk++) pa[kk] = ldg2nc_loop(hsrc(0) + (kk << 6), pol_el);
+                }
+                if (nH > 1) {
+#pragma unroll
+                    for (int kk = 0; kk < 4; kk++) pb2[kk] = ldg2nc_loop(hsrc(1) + (kk << 6), pol_el);
+                }
+                mbar_wait(sptr(&tbar[buf]), (unsigned)((gk >> 1) & 1));
+                __syncthreads();   // every warp is done with tile k-1: its buffer may be refilled
+                if (tid == 0 && k + 1 < nt) {
+                    fence_proxy_async();
+                    load_tile(k + 1, gk + 1);
+                }
+                const double *tq = tileq + (size_t)buf * BUFD;
+                Prog<WP> P;
+                {
+                    const uint64_t widx = (uint64_t)tidx << nW;
+                    const uint32_t o0 = __ldg(a.off16 + widx), ow = __ldg(a.off16 + widx + warp);
+                    const uint32_t nrec = (widx + nwarps < nwt ? __ldg(a.off16 + widx + nwarps) : a.total16) - o0;
+                    P.pg = (ST || nrec <= a.maxblk16) ? reinterpret_cast<const uint4 *>(tq + TS) + (ow - o0) : a.prog + ow;
+                    P.pl = s_pext + lane;
+                    P.pw = s_pextw + warp;
+                }
+                const int K = __popc(t);
+                if (K != curK) {
+                    flush();
+                    curK = K;
+                }
+                const int beta = cph ^ (K & 1) ^ par_t;
+                const int sh = beta ? 8 : 0;
+                const double mu_F = reinterpret_cast<const double *>(P.pg + 32)[0];
+
+                double qo[R], A[R], D[R], q[R];
+#pragma unroll
+                for (int kk = 0; kk < 4; kk++) {
+                    const double2 v = *reinterpret_cast<const double2 *>(tq + (jw | (kk << 6)));
+                    qo[2 * kk] = v.x;
+                    qo[2 * kk + 1] = v.y;
+                }
+#pragma unroll
+                for (int r = 0; r < R; r++) {
+                    A[r] = 0.0;
+                    D[r] = 0.0;
+                }
+                // ---- unit 0 (implied parity bit): busy in r iff b0(r) = beta ^ parity(r)
+                {
+                    const uint4 h0 = P.hdr(0);
+                    const double Wt = unit_rates(P, h0, sh, hdr_w0(h0), qo, A);
+                    const double We = beta ? Wt : 0.0, Wo = beta ? 0.0 : Wt;
+                    const double Ne = beta ? 0.0 : nu0, No = beta ? nu0 : 0.0;
+#pragma unroll
+                    for (int r = 0; r < R; r++) {
+                        const bool odd = (__popc(r) & 1) != 0;
+                        A[r] = fma(odd ? Wo : We, qo[r], A[r]);
+                        D[r] = fma(odd ? No : Ne, qo[r], D[r]);
+                    }
+                }
+                // ---- register units 1, 7, 8 (register bits 0, 1, 2)
+#pragma unroll
+                for (int rb = 0; rb < 3; rb++) {
+                    const int u = rb ? 6 + rb : 1;
+                    const int bit = 1 << rb;
+#pragma unroll
+                    for (int r = 0; r < R; r++) q[r] = qo[r ^ bit];
+                    const uint4 hu = P.hdr(u);
+                    const double Wt = unit_rates(P, hu, sh, hdr_w0(hu), q, A);
+                    const double nuu = a.nu[u];
+#pragma unroll
+                    for (int r = 0; r < R; r++) {
+                        if (r & bit) A[r] = fma(Wt, q[r], A[r]);
+                        else D[r] = fma(nuu, q[r], D[r]);
+                    }
+                }
+                // ---- lane units 2..6 (lane bits 0..4): busy per lane
+#pragma unroll
+                for (int b = 0; b < 5; b++) {
+                    const int u = 2 + b;
+                    const bool busy = (lane >> b) & 1;
+                    const uint32_t jn = jw ^ (2u << b);
+#pragma unroll
+                    for (int kk = 0; kk < 4; kk++) {
+                        const double2 v = *reinterpret_cast<const double2 *>(tq + (jn | (kk << 6)));
+                        q[2 * kk] = v.x;
+                        q[2 * kk + 1] = v.y;
+                    }
+                    const uint4 hu = P.hdr(u);
+                    const double Wt = unit_rates(P, hu, sh, busy ? hdr_w0(hu) : 0.0, q, A);
+                    const double wn = busy ? 0.0 : a.nu[u];
+#pragma unroll
+                    for (int r = 0; r < R; r++) {
+                        A[r] = fma(Wt, q[r], A[r]);
+                        D[r] = fma(wn, q[r], D[r]);
+                    }
+                }
+                // ---- warp units 9..8+nW (warp bits): busy per warp (uniform branch)
+                for (int b = 0; b < nW; b++) {
+                    const int u = 9 + b;
+                    const uint32_t jn = jw ^ (256u << b);
+#pragma unroll
+                    for (int kk = 0; kk < 4; kk++) {
+                        const double2 v = *reinterpret_cast<const double2 *>(tq + (jn | (kk << 6)));
+                        q[2 * kk] = v.x;
+                        q[2 * kk + 1] = v.y;
+                    }
+                    if ((warp >> b) & 1) {
+                        const uint4 hu = P.hdr(u);
+                        const double Wt = unit_rates(P, hu, sh, hdr_w0(hu), q, A);
+#pragma unroll
+                        for (int r = 0; r < R; r++) A[r] = fma(Wt, q[r], A[r]);
+                    } else {
+                        const double nuu = a.nu[u];
+#pragma unroll
+                        for (int r = 0; r < R; r++) D[r] = fma(nuu, q[r], D[r]);
+                    }
+                }
+                // ---- tile units (H): neighbour tile slices straight from global memory (L2), two
+                //      units of loads in flight; unrolled by two so the buffers alternate in place
+                auto unit_H = [&](int h, double2 (&buf)[4]) {
+                    const int u = NVU + h;
+#pragma unroll
+                    for (int kk = 0; kk < 4; kk++) {
+                        q[2 * kk] = buf[kk].x;
+                        q[2 * kk + 1] = buf[kk].y;
+                    }
+                    if (h + 2 < nH) {
+                        const double *src = hsrc(h + 2);
+#pragma unroll
+                        for (int kk = 0; kk < 4; kk++) buf[kk] = ldg2nc_loop(src + (kk << 6), pol_el);
+                    }
+                    if ((t >> h) & 1u) {
+                        const uint4 hu = P.hdr(u);
+                        const double Wt = unit_rates(P, hu, sh, hdr_w0(hu), q, A);
+#pragma unroll
+                        for (int r = 0; r < R; r++) A[r] = fma(Wt, q[r], A[r]);
+                    } else {
+                        const double nuu = a.nu[u];
+#pragma unroll
+                        for (int r = 0; r < R; r++) D[r] = fma(nuu, q[r], D[r]);
+                    }
+                };
+                for (int h = 0; h < nH; h += 2) {
+                    unit_H(h, pa);
+                    if (h + 1 < nH) unit_H(h + 1, pb2);
+                }
+                // ---- lambda_m: Lambda minus the atoms whose whole (truncated) list is busy
+                double lam[R];
+                if (FULL) {
+#pragma unroll
+                    for (int r = 0; r < R; r++) lam[r] = a.Lam;
+                } else {
+                    double one[R];
+#pragma unroll
+                    for (int r = 0; r < R; r++) {
+                        lam[r] = 0.0;
+                        one[r] = 1.0;
+                    }
+                    const uint4 hN = P.hdr(a.N);
+                    const double Bt = unit_rates(P, hN, sh, hdr_w0(hN), one, lam);
+#pragma unroll
+                    for (int r = 0; r < R; r++) lam[r] = a.Lam - (lam[r] + Bt);
+                }
+                // ---- epilogue (phase parameters read here, not held across the gather)
+                const int mode = vld(L3.mode);
+                const uint32_t active = vld(L3.active);
+                double *const Pc = a.pw + coff;
+                const double2 *const omk = a.omkap_all + coff;
+                const int base = K + popc_t;
+                const double mu_base = mu_F + mu_t;
+                double pnew[R];
+                bool act[R];
+                double bins[3][NB];
+#pragma unroll
+                for (int h = 0; h < 3; h++)
+#pragma unroll
+                    for (int v = 0; v < NB; v++) bins[h][v] = 0.0;
+#pragma unroll
+                for (int r = 0; r < R; r++) {
+                    const int pc = __popc(r);
+                    const int b0 = beta ^ (pc & 1);
+                    const int n = base + pc + b0;
+                    const double mu = mu_base + s_mr[r] + (b0 ? nu0 : 0.0);
+                    double lm = lam[r];
+                    if (FULL && n == a.N) lm = 0.0;
+                    const double den = lm + mu;
+                    const uint32_t j = jt + (jw | ((r >> 1) << 6) | (r & 1));
+                    // loads outside the mode branches (residual phases read omega/kappa unused)
+                    const double2 ok = ldg2p(omk + j, pol_ef);
+                    const double pold = mode >= 1 ? __ldcg(Pc + j) : 0.0;
+                    double val[NB];
+                    act[r] = true;
+                    if (mode == 2) {
+                        const double out = s_z[n] * pold * den;
+                        const double in = s_x[n] * A[r] + s_y[n] * D[r];
+                        val[0] = fabs(out - in);
+                        val[1] = out;
+#pragma unroll
+                        for (int v = 2; v < NB; v++) val[v] = 0.0;
+                        pnew[r] = 0.0;
+                    } else {
+                        act[r] = (active >> n) & 1u;
+                        const double p = (s_x[n] * A[r] + s_y[n] * D[r]) * rcp_nr(den);
+                        pnew[r] = p;
+                        val[0] = act[r] ? p : 0.0;
+                        val[1] = act[r] ? p * ok.x : 0.0;
+                        val[2] = act[r] ? p * ok.y : 0.0;
+                        int v = 3;
+                        if (!FULL) val[v++] = act[r] ? p * lm : 0.0;
+                        if (mode == 1 && act[r]) dsum = fma(s_w[n], fabs(p - pold), dsum);
+                    }
+                    // bin h(r) = (pc + 1 - beta) >> 1
+#pragma unroll
+                    for (int v = 0; v < NB; v++) {
+                        if (pc == 0) bins[0][v] += val[v];
+                        else if (pc == 2) bins[1][v] += val[v];
+                        else if (pc == 1) {
+                            if (beta) bins[0][v] += val[v];
+                            else bins[1][v] += val[v];
+                        } else {
+                            if (beta) bins[1][v] += val[v];
+                            else bins[2][v] += val[v];
+                        }
+                    }
+                }
+#pragma unroll
+                for (int h = 0; h < 3; h++)
+#pragma unroll
+                    for (int v = 0; v < NB; v++) sb[(h * NB + v) * nthr + tid] += bins[h][v];
+                if (mode < 2) {
+#pragma unroll
+                    for (int kk = 0; kk < 4; kk++) {
+                        double *dst = Pc + (jt + (jw | (kk << 6)));
+                        if (act[2 * kk] && act[2 * kk + 1]) {
+#ifndef HQ_NO_L2POL
+                            stg2_pol(dst, pnew[2 * kk], pnew[2 * kk + 1], pol_ef);
+#else
+                            *reinterpret_cast<double2 *>(dst) = make_double2(pnew[2 * kk], pnew[2 * kk + 1]);
+#endif
+                        } else {
+                            if (act[2 * kk]) dst[0] = pnew[2 * kk];
+                            if (act[2 * kk + 1]) dst[1] = pnew[2 * kk + 1];
+                        }
+                    }
+                }
+            }
+            g += (uint32_t)nt;
+            flush();
+            // ---- the check's |dp| total: warp sums, then warp 0 sums the warps in order
+            if (vld(L3.mode) == 1) {
+                const double ws = warp_sum(dsum);
+                if (lane == 0) s_red[warp] = ws;
+            }
+            // ---- CTA partials: warp w's lane L holds layer L; fixed-order sum over warps
+            __syncthreads();   // every copy consumed: reuse the tile buffers
+            double *red = tileq;
+#pragma unroll
+            for (int v = 0; v < NB; v++) red[((size_t)warp * 32 + lane) * NB + v] = acc[v];
+            __syncthreads();
+            if (warp == 0) {
+                double s[NB];
+#pragma unroll
+                for (int v = 0; v < NB; v++) s[v] = 0.0;
+                for (int w = 0; w < (int)nwarps; w++)
+#pragma unroll
+                    for (int v = 0; v < NB; v++) s[v] += red[((size_t)w * 32 + lane) * NB + v];
+                // this CTA's sums into the phase buffer (exact; lane L: layer L)
+                unsigned long long *xg = a.xg + (size_t)vld(L3.pbuf) * (HQ_NL * HQ_NX * HQ_XL);
+                const bool res = vld(L3.mode) == 2;
+                bool ok = true;
+                if (lane <= a.N) {
+#pragma unroll
+                    for (int v = 0; v < NB; v++) {
+                        if (res && v >= 2) break;
+                        const int slot = res ? XV_RNUM + v : SL::slot(v);
+                        ok = xadd_g(xg + ((size_t)lane * HQ_NX + slot) * HQ_XL, s[v], a.xe) && ok;
+                    }
+                }
+                if (vld(L3.mode) == 1 && lane == 0) {
+                    double ds = 0.0;
+                    for (int w = 0; w < (int)nwarps; w++) ds += s_red[w];
+                    ok = xadd_g(xg + (size_t)V2_DL1 * HQ_XL, ds, a.xe) && ok;
+                }
+                if (!ok) atomicOr(&a.ctl->err, 1);
+            }
+            __syncthreads();
+        }
+        // CTA 0 clears the buffer of the next phase (= phase - 2 mod 3: read by every CTA before
+        // the previous barrier, written only after this one)
+        if (blockIdx.x == 0)
+            for (int i = tid; i < HQ_NL * HQ_NX * HQ_XL; i += blockDim.x)
+                a.xg[(size_t)((L3.pbuf + 1) % 3) * (HQ_NL * HQ_NX * HQ_XL) + i] = 0ull;
+        __threadfence();
+        grid.sync();
+        // ---- the scalar step / residual and the control decision, identically in every CTA
+        const int kind = L3.kind;
+        const unsigned long long *xg = a.xg + (size_t)L3.pbuf * (HQ_NL * HQ_NX * HQ_XL);
+        double num = 0.0, den = 0.0;
+        if (kind == K3_SWEEP) {
+            for (int i = tid; i < (a.N + 1) * NV2; i += blockDim.x) {
+                const int L = i / NV2, v = i - L * NV2;
+                s_S[L][v] = xget(xg + ((size_t)L * HQ_NX + v) * HQ_XL, a.xe);
+            }
+            if (tid == 0) s_red[0] = xget(xg + (size_t)V2_DL1 * HQ_XL, a.xe);   // |dp| total of this phase
+            __syncthreads();
+            scalars_update(a.N, a.full_lists, a.Lam, 1, L3.c, L3.active, s_S, s_blk);
+            // convergence proxy: sum over the two check half-sweeps of
+            // p(n) |dp| (p(n) of the phase's start) -- the current and the previous phase
+            if (tid == 0) {
+                s_blk[V2S_MISC + 2] = s_red[0] + L3.dprev;
+                L3.dprev = L3.mode == 1 ? s_red[0] : 0.0;
+            }
+        } else {
+            for (int i = tid; i <= a.N; i += blockDim.x) {
+                s_blk[V2S_RNUM + i] = xget(xg + ((size_t)i * HQ_NX + XV_RNUM) * HQ_XL, a.xe);
+                s_blk[V2S_RDEN + i] = xget(xg + ((size_t)i * HQ_NX + XV_RDEN) * HQ_XL, a.xe);
+            }
+            __syncthreads();
+            for (int L = 0; L <= a.N; L++) {
+                num += s_blk[V2S_RNUM + L];
+                den += s_blk[V2S_RDEN + L];
+            }
+        }
+        if (tid == 0) {
+            const int gerr = *(volatile int *)&a.ctl->err;
+            if (blockIdx.x == 0) {
+                unsigned long long tp1;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tp1));
+                if (kind == K3_SWEEP) L3.ns_sweep += tp1 - L3.tp0;
+                else L3.ns_res += tp1 - L3.tp0;
+            }
+            if (kind != K3_SWEEP) s_blk[V2S_MISC + 1] = num / den;
+            loop3_control(a, s_blk, num, den, gerr);
+            L3.pbuf = (L3.pbuf + 1) % 3;
+        }
+    }
+    // ---- exit: CTA 0 publishes the scalar block and the counters
+    if (blockIdx.x == 0) {
+        for (int i = tid; i < V2S_TOTAL; i += blockDim.x) a.blk[i] = s_blk[i];
+        if (tid == 0) {
+            Ctl3 *o = a.ctl;
+            o->status = L3.status == SOLVE3_RUNNING ? SOLVE3_MAXITER : L3.status;
+            o->sweeps = L3.sweeps;
+            o->halfsweeps = L3.halfsweeps;
+            o->nres = L3.nres;
+            o->phases = L3.phases;
+            o->updates = L3.updates;
+            o->res = L3.res;
+            o->proxy = L3.proxy;
+            o->ns_sweep = L3.ns_sweep;
+            o->ns_res = L3.ns_res;
+        }
+    }
+}
 // ---------------------------------------------------------------------------
 // Rate-program precompute (once per instance): Algorithm 3
 // walked symbolically over the tile's varying units.
@@ -868,17 +1693,25 @@ __device__ int tile_program(const P3Args &a, uint32_t t, double *W0, PairAcc3 &P
     // records: per unit with data: a table if it has thread-conditioned pairs, then one
     // group per distinct rm; a table over the lane/warp bits M its conditions use has
     // 2^|M| entries (ceil(2^|M| / 2) records); a group adds one header record
+    // (groups whose table would have one entry -- register-dependent pairs with no lane / warp
+    // condition, M = 0 -- are merged into the unit's register table instead: 8 records,
+    // the summed rate of each register state for beta = 0 and beta = 1)
     int nrec = 0;
     int k = 0;
     while (k < P.n) {
         const int u = (int)(P.key[k] & 63);
-        const uint16_t rm = P.rm[k];
-        uint32_t M = own_bits(a, u);
-        while (k < P.n && (int)(P.key[k] & 63) == u && P.rm[k] == rm) {
-            M |= cond_bits(a, P.key[k] >> 6);
-            k++;
+        bool rtab = false;
+        while (k < P.n && (int)(P.key[k] & 63) == u) {
+            const uint16_t rm = P.rm[k];
+            uint32_t M = own_bits(a, u);
+            while (k < P.n && (int)(P.key[k] & 63) == u && P.rm[k] == rm) {
+                M |= cond_bits(a, P.key[k] >> 6);
+                k++;
+            }
+            if (rm && M == 0u) rtab = true;
+            else nrec += (rm ? 1 : 0) + (((1 << __popc(M)) + 1) >> 1);
         }
-        nrec += (rm ? 1 : 0) + (((1 << __popc(M)) + 1) >> 1);
+        if (rtab) nrec += 8;
     }
     return nrec;
 }
@@ -957,6 +1790,44 @@ __global__ void k_prog_write3(P3Args a, const uint32_t *__restrict__ order, cons
             const uint32_t own = own_bits(a, u);
             const uint32_t start = pos;
             uint32_t inf = 0u, ng = 0u;
+            // pass 1: register table of the lane-uniform register-dependent groups (M = 0),
+            // placed after the lane table (written in pass 2 at `start`)
+            int kend = k;
+            uint32_t tab_recs = 0;   // records of the lane table (rm = 0 pairs), if any
+            bool rtab = false;
+            while (kend < P.n && (int)(P.key[kend] & 63) == u) {
+                const uint16_t rm = P.rm[kend];
+                uint32_t M = own;
+                int k1 = kend;
+                while (k1 < P.n && (int)(P.key[k1] & 63) == u && P.rm[k1] == rm) {
+                    M |= cond_bits(a, P.key[k1] >> 6);
+                    k1++;
+                }
+                if (!rm) tab_recs = (uint32_t)(((1 << __popc(M)) + 1) >> 1);
+                else if (M == 0u) rtab = true;
+                kend = k1;
+            }
+            if (rtab) {
+                double *wr = reinterpret_cast<double *>(data + start + tab_recs);   // [beta][r]
+                for (int e = 0; e < 16; e++) wr[e] = 0.0;
+                int k1 = k;
+                while (k1 < kend) {
+                    const uint16_t rm = P.rm[k1];
+                    uint32_t M = own;
+                    int k2 = k1;
+                    while (k2 < kend && P.rm[k2] == rm) {
+                        M |= cond_bits(a, P.key[k2] >> 6);
+                        k2++;
+                    }
+                    if (rm && M == 0u)
+                        for (int kk = k1; kk < k2; kk++)
+                            for (int e = 0; e < 16; e++)
+                                if ((rm >> e) & 1u) wr[e] += P.val[kk];
+                    k1 = k2;
+                }
+                inf |= 1u << 30;
+            }
+            // pass 2: the lane table and the remaining groups
             while (k < P.n && (int)(P.key[k] & 63) == u) {
                 const uint16_t rm = P.rm[k];
                 const int k0 = k;
@@ -965,6 +1836,8 @@ __global__ void k_prog_write3(P3Args a, const uint32_t *__restrict__ order, cons
                     M |= cond_bits(a, P.key[k] >> 6);
                     k++;
                 }
+                if (rm && M == 0u) continue;   // in the register table
+                if (rm && pos == start + tab_recs && rtab) pos += 8;   // skip over the register table
                 // table over the thread bits M: entry idx holds the value of every thread
                 // whose M-bits are pdep(idx, M); a pair applies when its lane / warp units
                 // (and, for a lane or warp unit, the unit itself) are busy for the thread
@@ -993,7 +1866,8 @@ __global__ void k_prog_write3(P3Args a, const uint32_t *__restrict__ order, cons
                 if (ne & 1) tab[ne] = 0.0;
                 pos += (uint32_t)((ne + 1) >> 1);
             }
-            if (ng > 255 || start > 0xffffu) atomicExch(err, 3);
+            if (rtab && pos == start + tab_recs) pos += 8;   // register table last
+            if (ng > 255 || start > 0x3fffffu) atomicExch(err, 3);
             info[u] = inf | ng | (start << 8);
         }
         for (int u = 0; u < 32; u++) {
@@ -1038,11 +1912,18 @@ size_t sweep_smem(int nW, uint32_t maxblk16, int nslots) {
 // CTAs resident per SM the grid is sized for (hq_create: sgrid = nsm * ctas_per_sm)
 int ctas_per_sm(int nW) { return std::max(1, 16 >> nW); }
 
+// dynamic shared memory of k_loop3: the sweep kernel's, then this CTA's scalar block and the
+// phase sums
+size_t loop_smem(int nW, uint32_t maxblk16) {
+    return sweep_smem(nW, maxblk16, 0) + 8 * (size_t)(V2S_TOTAL + HQ_NL * NV2);
+}
+
 // staged program capacity (records per tile block): as large as fits, at most the largest
-// block (measured: staging every program beats more resident CTAs per SM)
+// block (measured: staging every program beats more resident CTAs per SM); sized for the
+// device-resident solve (loop_smem >= sweep_smem)
 uint32_t choose_cap(int nW, uint32_t maxblk16) {
     const size_t budget = 224u * 1024u - 2048u;
-    const size_t fixed = sweep_smem(nW, 0, 0);
+    const size_t fixed = loop_smem(nW, 0);
     if (fixed >= budget) return 0;
     const size_t cap = (budget - fixed) / (2 * 16);
     return (uint32_t)std::min<size_t>(cap, maxblk16);
@@ -1092,6 +1973,44 @@ static cudaError_t sweep_wp(const S3Args &a, int full, int mode, int grid, cudaS
 
 cudaError_t sweep(const S3Args &a, int full, int mode, int grid, cudaStream_t s) {
     return a.warp_programs ? sweep_wp<true>(a, full, mode, grid, s) : sweep_wp<false>(a, full, mode, grid, s);
+}
+
+template <bool FULL, bool WP, bool ST>
+static cudaError_t loop_launch(const S3Args &a, int grid, cudaStream_t s, int *occ) {
+    const size_t sm = loop_smem(a.nW, a.maxblk16);
+    auto kern = hq3::k_loop3<FULL, WP, ST>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    const int carve = (int)std::min<size_t>(100, (sm + 4096) * 100 / (228 * 1024) + 1);
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
+    if (e != cudaSuccess) return e;
+    if (occ) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, kern, 32 << a.nW, sm);
+    S3Args arg = a;
+    void *args[] = {(void *)&arg};
+    return cudaLaunchCooperativeKernel((const void *)kern, dim3(grid), dim3(32 << a.nW), args, sm, s);
+}
+
+template <bool WP, bool ST>
+static cudaError_t loop_st(const S3Args &a, int full, int grid, cudaStream_t s, int *occ) {
+    return full ? loop_launch<true, WP, ST>(a, grid, s, occ) : loop_launch<false, WP, ST>(a, grid, s, occ);
+}
+template <bool WP>
+static cudaError_t loop_wp(const S3Args &a, int full, int grid, cudaStream_t s, int *occ) {
+    return a.all_staged ? loop_st<WP, true>(a, full, grid, s, occ) : loop_st<WP, false>(a, full, grid, s, occ);
+}
+
+cudaError_t loop(const S3Args &a, int full, int grid, cudaStream_t s) {
+    return a.warp_programs ? loop_wp<true>(a, full, grid, s, nullptr) : loop_wp<false>(a, full, grid, s, nullptr);
+}
+
+int loop_occupancy(const S3Args &a, int full) {
+    int occ = 0;
+    const cudaError_t e = a.warp_programs ? loop_wp<true>(a, full, 0, 0, &occ) : loop_wp<false>(a, full, 0, 0, &occ);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return occ;
 }
 
 }  // namespace hq3_launch

@@ -24,15 +24,33 @@
 
 // rate program of a warp tile or of a CTA tile (16-byte records):
 //   [0..31]  per unit u (u = N: blocked pseudo-unit): {info, M, W0 lo, W0 hi}
-//            info = table << 31 | start << 8 | n_group (0: no data, W0 alone applies);
+//            info = table << 31 | rtab << 30 | start << 8 | n_group (0: no data, W0 alone
+//            applies); rtab: a register table follows the lane table (8 records: the summed
+//            rate of the register-dependent pairs without lane / warp condition, per register
+//            state r, for beta = 0 (records 0..3) and beta = 1 (records 4..7));
 //            M = thread bits the unit's table is indexed by (lane bits 0..4, warp bits 5..8);
 //            W0 = the tile-uniform rate of the unit
 //   [32]     {mu_F lo, mu_F hi, has, 0}: mu_F = sum of nu over the busy tile units
 //   data     per unit with data, at record 33 + start: a table of 2^|M| fp64 entries (if
-//            info >> 31), then n_group groups, each a header {rm | M_g << 16, 0, 0, 0} and a
+//            info >> 31), the register table (if rtab), then n_group groups, each a header {rm | M_g << 16, 0, 0, 0} and a
 //            table of 2^|M_g| entries; rm = admissible register states for beta = 0
 //            (bits 0..7) and beta = 1 (bits 8..15).  A thread's entry is pext(thread bits, M).
 // The programs of the warp tiles of a CTA tile (or its one CTA program) are contiguous.
+
+// ---- device-resident solve (k_loop3): control block and exact phase sums
+// Nonnegative per-layer sums in fixed point: HQ_XL 32-bit limbs in 64-bit words, unit
+// 2^(xe - 32 HQ_XL); three rotating phase buffers.
+#define HQ_XL 5
+#define HQ_NX 8      // value slots: V2_P, V2_OM, V2_KA, V2_LAM, V2_DL1, residual num, den, -
+enum { XV_RNUM = 5, XV_RDEN = 6 };
+#define HQ_XG_WORDS (3 * HQ_NL * HQ_NX * HQ_XL)
+struct Ctl3 {                    // written by CTA 0 when k_loop3 exits (host reads it once)
+    int status;                  // SOLVE3_*
+    int sweeps, halfsweeps, nres, phases, err;
+    double updates, res, proxy;
+    unsigned long long ns_sweep, ns_res;
+};
+enum { SOLVE3_RUNNING = 0, SOLVE3_CONVERGED = 1, SOLVE3_MAXITER = 2, SOLVE3_NUMERIC = 3, SOLVE3_NOTDECR = 4 };
 
 struct S3Args {
     int N;
@@ -68,6 +86,15 @@ struct S3Args {
     uint32_t prev_active;
     const double *prev_partial;
     double *blk_out;
+    // device-resident solve (k_solve3): both classes, the control block, exact sums
+    double *pw;                  // [2^N] both classes (class 0 first)
+    const double2 *omkap_all;    // [2^N] scatter weights of both classes
+    double *blk;                 // scalar block: the init block in, the final block out
+    unsigned long long *xg;      // [HQ_XG_WORDS] exact phase sums (host zeroes them)
+    Ctl3 *ctl;
+    int xe;                      // fixed-point exponent of the exact sums
+    double tol;
+    int max_iter;
 };
 
 struct P3Args {   // program precompute (one program per warp tile or per CTA tile)
@@ -96,6 +123,11 @@ cudaError_t prog_count(const P3Args &a, const uint32_t *order, uint32_t *size16,
 cudaError_t prog_write(const P3Args &a, const uint32_t *order, const uint32_t *off16, uint4 *prog, int *err,
                        int grid, cudaStream_t s);
 cudaError_t sweep(const S3Args &a, int full, int mode, int grid, cudaStream_t s);
+// device-resident solve (k_loop3): one cooperative launch runs every half-sweep, the
+// convergence checks and the verification residual; grid = the CTA ranges (a.range)
+cudaError_t loop(const S3Args &a, int full, int grid, cudaStream_t s);
+int loop_occupancy(const S3Args &a, int full);   // co-resident CTAs per SM (0: does not fit)
+size_t loop_smem(int nW, uint32_t maxblk16);
 size_t sweep_smem(int nW, uint32_t maxblk16, int nslots);
 int choose_slots(int nW, uint32_t maxblk16);
 uint32_t choose_cap(int nW, uint32_t maxblk16);

@@ -100,13 +100,58 @@ def test_mid_sizes_whole_vector(hq, N, cfg, J, L):
     whole_vector(g, o, inst)
 
 
+def gpu_solve_loop(hq, inst, loop):
+    """gpu_solve with the host-looped or the device-resident solve (HQ_LOOP is read at hq_create)."""
+    old = os.environ.get("HQ_LOOP")
+    os.environ["HQ_LOOP"] = loop
+    try:
+        g = gpu_solve(hq, inst)
+    finally:
+        if old is None:
+            os.environ.pop("HQ_LOOP")
+        else:
+            os.environ["HQ_LOOP"] = old
+    assert g["stats"]["device_loop"] == (1.0 if loop == "device" else 0.0)
+    return g
+
+
 def test_cfg3_whole_vector(hq):
-    """cfg3 (N = 24, 16.8M states): the oracle run in the session, every state compared."""
+    """cfg3 (N = 24, 16.8M states): the oracle run in the session, every state compared, for
+    both the host-looped and the device-resident solve (one cooperative launch)."""
     inst = hqinst.config_instance(3)
-    g = gpu_solve(hq, inst)
     o = oracle.solve(inst, tol=TOL, max_iter=5000)
     assert o["status"] == 0
-    whole_vector(g, o, inst)
+    for loop in ("host", "device"):
+        g = gpu_solve_loop(hq, inst, loop)
+        whole_vector(g, o, inst)
+
+
+@pytest.mark.parametrize("N,cfg,J", [(12, 2, 60), (18, 2, 100), (21, 4, 150)])
+def test_device_loop_matches_host_loop(hq, N, cfg, J):
+    """The device-resident solve performs the same half-sweeps as the host-looped one: after a
+    fixed number of sweeps (tol = 0) the iterates agree to rounding (the per-layer sums are
+    added in a different order), and both converge to the oracle's pi."""
+    inst = hqinst.config_instance(cfg, N=N, J=J)
+    for K in (1, 7):
+        its = []
+        for loop in ("host", "device"):
+            old = os.environ.get("HQ_LOOP")
+            os.environ["HQ_LOOP"] = loop
+            try:
+                s = hq.Solver.from_instance(inst)
+            finally:
+                if old is None:
+                    os.environ.pop("HQ_LOOP")
+                else:
+                    os.environ["HQ_LOOP"] = old
+            r = s.solve(tol=0.0, max_iter=K)
+            assert r["iters"] == K and s.stats()["device_loop"] == (1.0 if loop == "device" else 0.0)
+            its.append(r["pi"].cpu().numpy())
+            s.close()
+        assert np.abs(its[0] - its[1]).max() <= 1e-14
+    o = oracle.solve(inst, tol=TOL)
+    for loop in ("host", "device"):
+        whole_vector(gpu_solve_loop(hq, inst, loop), o, inst)
 
 
 def test_cfg4_against_oracle_fixture(hq):
