@@ -87,9 +87,28 @@ hq_status hq_create(int N, int J, const double *lambda, const double *mu, const 
  *   iters_out    host: sweeps performed.
  *   residual_out host: the true r(pi) of the returned pi (not a proxy).
  *
+ * Execution: N >= 9 runs the CTA-tiled sweep kernel; for N < 21
+ * the whole loop -- every half-sweep, the convergence checks and the verification
+ * residual -- is ONE cooperative launch (device-resident; the host synchronises
+ * once), for N >= 21 one launch per half-sweep with host-scheduled checks (the
+ * faster path there); HQ_LOOP=device|host in the environment at hq_create forces
+ * either.  An instance whose per-tile rate programs exceed their format (more than
+ * 2048 distinct (unit, condition) pairs in a tile, e.g. thousands of unstructured
+ * lists) falls back to the general two-pass path (per-thread trie walk; slower).
+ *
+ * Device memory (allocated at the first hq_solve, from the CUDA memory pool):
+ * 8 B/state for the conditional probabilities p_n + 16 B/state of scatter weights
+ * (+ 8 B/state of lambda_m for truncated lists) + the rate programs (hq_stats [12];
+ * about 4 B/state at the BASELINE configs) + small tables, i.e. about 28-36 B x 2^N
+ * (75-77 GB at N = 31), plus the caller's pi (8 B x 2^N).  N is at most 31
+ * (HQ_MAXN); HQ_E_NOMEM if the working set does not fit the free device memory.
+ *
  * The call synchronises cuda_stream before returning.
  * Returns HQ_OK, HQ_NOT_CONVERGED (pi, iters, residual hold the last
- * iterate), HQ_E_INVAL, HQ_E_NOMEM, HQ_E_CUDA or HQ_E_NUMERIC.
+ * iterate), HQ_E_INVAL, HQ_E_NOMEM, HQ_E_CUDA or HQ_E_NUMERIC (a non-positive or
+ * non-finite layer normaliser, a non-finite sum, or a convergence proxy that grew by
+ * more than 1.5x at four consecutive checks: the iteration diverges -- Assumption 1,
+ * PAPER.md:359-367, is not guaranteed for every instance).
  */
 hq_status hq_solve(hq_handle h, double tol, int max_iter, double *pi, void *cuda_stream, int *iters_out,
                    double *residual_out);

@@ -101,6 +101,10 @@ int tile_states();
 cudaError_t init_v2(const KArgs &k, int grid, cudaStream_t s);
 }  // namespace hqk_launch
 
+// internal status (never returned by the ABI): an instance whose rate programs do not fit the
+// tiled paths' format; hq_solve falls back to path 1 (per-thread trie walk, any instance)
+static const hq_status HQ_I_OVERFLOW = (hq_status)-100;
+
 namespace {
 
 thread_local std::string g_create_error;
@@ -824,7 +828,7 @@ static hq_status v2_prepare(hq_problem *h, cudaStream_t s) {
     }
     if (herr) {
         h->err = "rate program overflow (too many distinct (unit, pattern) pairs in a tile)";
-        return HQ_E_NUMERIC;
+        return HQ_I_OVERFLOW;
     }
     const uint64_t total16 = (uint64_t)last[0] + last[1];
     h->total16 = (uint32_t)total16;
@@ -839,7 +843,7 @@ static hq_status v2_prepare(hq_problem *h, cudaStream_t s) {
         HQ_CUDA(cudaStreamSynchronize(s));
         if (herr) {
             h->err = "rate program overflow (more than 255 lane-only pairs or groups for a unit)";
-            return HQ_E_NUMERIC;
+            return HQ_I_OVERFLOW;
         }
     }
     else HQ_CUDA(hq2_launch::prog_write(pa, h->d_order, h->d_off16, h->d_prog, g, s));
@@ -960,7 +964,7 @@ static hq_status v3_programs(hq_problem *h, cudaStream_t s, int nwv, const std::
     if (herr) {
         cleanup();
         h->err = "rate program overflow (too many distinct (unit, pattern) pairs in a tile)";
-        return HQ_E_NUMERIC;
+        return HQ_I_OVERFLOW;
     }
     const uint64_t total16 = (uint64_t)offp[nprog - 1] + sz[nprog - 1];
     if (total16 >= (1ull << 32)) {
@@ -1043,7 +1047,7 @@ static hq_status v3_programs(hq_problem *h, cudaStream_t s, int nwv, const std::
     if (herr) {
         ps.release();
         h->err = "rate program overflow (more than 255 groups for a unit)";
-        return HQ_E_NUMERIC;
+        return HQ_I_OVERFLOW;
     }
     ps.cap = hq3_launch::choose_cap(nW, ps.maxblk);
     return HQ_OK;
@@ -1340,7 +1344,7 @@ static hq_status solve_v2(hq_problem *h, double tol, int max_iter, double *pi, c
     // convergence checks: the two half-sweeps before a check record |dp|
     int next_check = N + 2 * 12;
     double prev_proxy = -1.0;
-    int prev_check = 0;
+    int prev_check = 0, rise = 0;
     for (int t = 1; N >= 2; t++) {
         uint32_t active = 0;
         for (int n = 1; n <= N - 1; n++)
@@ -1397,6 +1401,13 @@ static hq_status solve_v2(hq_problem *h, double tol, int max_iter, double *pi, c
         }
         double rate = 0.0;   // per half-sweep decay factor
         if (prev_proxy > 0.0 && t > prev_check) rate = std::pow(proxy / prev_proxy, 1.0 / (t - prev_check));
+        // divergence guard (Assumption 1, can fail): the proxy grew by > 1.5x
+        // at four consecutive checks
+        rise = (prev_proxy > 0.0 && proxy > 1.5 * prev_proxy) ? rise + 1 : 0;
+        if (rise >= 4) {
+            h->err = "the residual proxy grew at four consecutive convergence checks (iteration diverges)";
+            return HQ_E_NUMERIC;
+        }
         prev_proxy = proxy;
         prev_check = t;
         double level = proxy;
@@ -1556,6 +1567,22 @@ static hq_status solve_dev(hq_problem *h, double tol, int max_iter, double *pi, 
     return HQ_OK;
 }
 
+// Switch a handle to path 1 (two-pass kernels, per-thread trie walk over the ABI-ordered
+// preference trie): used when the tiled paths' rate programs overflow their format
+// (more than V3_MAXPAIRS distinct (unit, pattern) pairs in a tile, e.g. thousands of
+// unstructured lists).  Slower, but valid for every instance.
+static void fallback_path1(hq_problem *h) {
+    h->release();
+    h->device = -1;
+    h->path = 1;
+    h->v2 = false;
+    h->dev_loop = false;
+    h->chunked = false;
+    for (int u = 0; u < h->N; u++) h->perm[u] = u;
+    h->trie = build_trie(h->N, h->J, h->lam.data(), h->pref.data());
+    h->nu_int = h->mu;
+}
+
 static hq_status solve_core(hq_handle h, double tol, int max_iter, double *pi, void *cuda_stream, int *iters_out,
                             double *residual_out) {
     if (!h) return HQ_E_INVAL;
@@ -1583,6 +1610,10 @@ static hq_status solve_core(hq_handle h, double tol, int max_iter, double *pi, v
         if (st != HQ_OK) {
             cudaEventDestroy(a0);
             cudaEventDestroy(a1);
+            if (st == HQ_I_OVERFLOW) {   // rate programs do not fit: the general path for this handle
+                fallback_path1(h);
+                return solve_core(h, tol, max_iter, pi, cuda_stream, iters_out, residual_out);
+            }
             return st;
         }
         HQ_CUDA(cudaEventRecord(a1, s));

@@ -160,3 +160,19 @@ def test_measures_before_solve_is_order_error(hq):
         s.measures(pi)
     assert ei.value.status == hq.HQ_E_ORDER
     s.close()
+
+
+def test_rate_program_overflow_falls_back(hq):
+    """Thousands of unstructured (random) full lists: the tiled paths' rate programs would hold
+    more than V3_MAXPAIRS distinct (unit, pattern) pairs in a tile; hq_solve falls back to the
+    general path (per-thread trie walk, stats path 1) instead of failing, and still matches the
+    oracle."""
+    N, J = 12, 4000
+    rng = np.random.default_rng(2026)
+    pref = np.array([rng.permutation(N) for _ in range(J)], dtype=np.int32)
+    lam = rng.dirichlet(np.ones(J)) * 0.7 * N
+    inst = hqinst.from_arrays(lam, np.ones(N) + rng.random(N), pref, name="random-lists")
+    g = gpu_solve(hq, inst)
+    assert g["stats"]["path"] == 1
+    o = oracle.solve(inst, tol=TOL)
+    check_parity(g, o, inst)
