@@ -383,7 +383,6 @@ struct hq_problem {
     bool v2 = false, v2_ready = false;
     int path = 1;                  // 1: N < 8 two-pass, 2: warp-tiled (hq_v2.cu), 3: CTA-tiled (hq_v3.cu)
     int nW = 0;                    // path 3: log2(warps per CTA)
-    int nslots = 0;                // path 3: CTA ring slots
     uint32_t maxblk_all = 0;       // path 3: largest program block of a CTA tile (records)
     unsigned long long *d_wtime = nullptr;   // path 3: per-warp busy cycles (-DHQ_WARP_TIMING builds)
     int prog_nwv = 0;              // path 3: warp bits varying inside a rate program (nW: CTA programs)
@@ -819,10 +818,9 @@ static hq_status v2_prepare(hq_problem *h, cudaStream_t s) {
     dfree(d_max);
     if (h->path == 3) {   // staged program capacity; larger blocks are read from global memory
         h->maxblk_all = h->maxrec;
-        h->maxrec = hq3_launch::choose_cap(h->nW, h->maxrec);
-        h->nslots = hq3_launch::choose_slots(h->nW, h->maxrec);
+        h->maxrec = hq3_launch::choose_cap(h->nW, h->maxrec, h->dev_loop);
     }
-    if (h->path == 3 ? h->nslots < 1 : hq2_launch::sweep_smem(h->maxrec) > 150u * 1024u) {
+    if (h->path == 3 ? !hq3_launch::fits_smem(h->nW, h->maxrec, h->dev_loop) : hq2_launch::sweep_smem(h->maxrec) > 150u * 1024u) {
         h->err = "rate program of a tile exceeds the shared-memory budget";
         return HQ_E_NUMERIC;
     }
@@ -1049,7 +1047,7 @@ static hq_status v3_programs(hq_problem *h, cudaStream_t s, int nwv, const std::
         h->err = "rate program overflow (more than 255 groups for a unit)";
         return HQ_I_OVERFLOW;
     }
-    ps.cap = hq3_launch::choose_cap(nW, ps.maxblk);
+    ps.cap = hq3_launch::choose_cap(nW, ps.maxblk, h->dev_loop);
     return HQ_OK;
 }
 
@@ -1186,8 +1184,7 @@ static hq_status v3_prepare(hq_problem *h, cudaStream_t s) {
     hq_status st = v3_programs(h, s, cta_prog ? h->nW : 0, order, a);
     if (st != HQ_OK) return st;
     if (a.prog) use_progset(h, a);
-    h->nslots = hq3_launch::choose_slots(h->nW, h->maxrec);
-    if (h->nslots < 1) {
+    if (!hq3_launch::fits_smem(h->nW, h->maxrec, h->dev_loop)) {
         h->err = "tile working set exceeds the shared-memory budget";
         return HQ_E_NUMERIC;
     }
@@ -1219,7 +1216,6 @@ static cudaError_t tiled_sweep(hq_problem *h, const S2Args &sa, int mode, cudaSt
     a.prog = sa.prog;
     a.total16 = sa.total16;
     a.maxblk16 = sa.maxrec;
-    a.nslots = h->nslots;
     a.range = h->d_range;
     a.full_lists = sa.full_lists;
     a.warp_programs = (h->prog_nwv == 0) ? 1 : 0;

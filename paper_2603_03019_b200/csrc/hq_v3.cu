@@ -14,13 +14,12 @@
 //   * register bits (units 1, 7, 8) come from the thread's own registers,
 //   * the implied parity unit 0 is the state's own index in the other class,
 //   * lane and warp bits (units 2..6, 9..8+nW) come from the tile's block of q,
-//     staged in shared memory (double-buffered across tiles) by bulk copies
-//     (cp.async.bulk, the TMA engine) completed on an mbarrier,
-//   * tile bits ("H" units) come from the neighbour tiles' blocks, streamed
-//     through a CTA-wide ring of tile-sized slots: the last warp to release a
-//     slot refills it with the block needed nslots items later.
-// The same ring streams the own old p (convergence proxy / residual) and the
-// scatter weights (omega, kappa) of the tile.
+//     staged in shared memory (double-buffered across tiles) with the tile's rate
+//     program by bulk copies (cp.async.bulk, the TMA engine) completed on an mbarrier,
+//   * tile bits ("H" units) come from the neighbour tiles' blocks in global memory
+//     (L2): coalesced 16-byte loads, two units ahead of the one accumulated.
+// The scatter weights (omega, kappa) and the old p (checks, residual) are read per
+// state in the epilogue.
 //
 // Upward rates come from a per-tile "rate program" (Algorithm 3,
 // PAPER.md:541-567, evaluated symbolically for the 2^T states of the tile):
@@ -29,9 +28,10 @@
 // pairs sharing one mask of admissible register states.
 //
 // Per-layer sums (sum p, sum p omega, sum p kappa [, sum p lambda_m]
-// [, sum |dp|]) are accumulated in fixed order: per-thread bins, warp
-// butterflies keyed by layer when popcount(tile) changes, a fixed-order sum
-// over the warps of the CTA, and k_scalars2's fixed-order sum over CTAs.
+// [, sum |dp|]) are accumulated in fixed order: per-thread bins, a per-warp flush
+// keyed by layer when popcount(tile) changes (flush_fast3), a fixed-order sum
+// over the warps of the CTA, then either k_scalars2's fixed-order sum over CTAs
+// (host loop) or exact fixed-point atomics (device loop, k_loop3).
 #include <cuda_runtime.h>
 #include <cooperative_groups.h>
 #include <cstdint>
@@ -351,6 +351,67 @@ __device__ __forceinline__ void load_coef3(const double *coef) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// Flush of the per-thread layer bins of one tile popcount K into the per-lane layer
+// accumulators (warp w, lane L: layer L).  Bin h of lane l holds relative layer y = z(l) + h
+// (layer L0 + 2y), z(l) = ceil(popc(l) / 2) if p0 = 0 else floor(popc(l) / 2): at most 32
+// (lane, h) entries per y.  Five lanes share each y (lanes 5y .. 5y + 4 take every fifth
+// entry in ascending (lane, h) order), then lane 5y adds the five shares in lane order:
+// a fixed summation order (bitwise reproducible).  The per-lane entry lists come from a
+// table built once per CTA: byte k of s_fl[p0][lane] is the k-th scratch offset (l * 3 + h),
+// byte 7 the count (<= 7).
+// ---------------------------------------------------------------------------
+__device__ void flush_table3(uint64_t *tab) {   // one warp
+    const int lane = threadIdx.x & 31;
+    for (int p0 = 0; p0 < 2; p0++) {
+        uint64_t desc = 0;
+        if (lane < 30) {
+            const int y = lane / 5, q = lane % 5;
+            int idx = 0, k = 0;
+            for (int l = 0; l < 32; l++) {
+                const int z = p0 ? __popc(l) / 2 : (__popc(l) + 1) / 2;
+                for (int h = 0; h < 3; h++)
+                    if (z + h == y) {
+                        if (idx % 5 == q && k < 7) desc |= (uint64_t)(l * 3 + h) << (8 * k++);
+                        idx++;
+                    }
+            }
+            desc |= (uint64_t)k << 56;
+        }
+        tab[p0 * 32 + lane] = desc;
+    }
+}
+
+template <int NB>
+__device__ __forceinline__ void flush_fast3(const uint64_t *tab, int p0, int L0, int lane, int tid, int nthr,
+                                            double *sb, double *fscr, double (&acc)[NB]) {
+    const uint64_t desc = tab[p0 * 32 + lane];
+    const int cnt = (int)(desc >> 56);
+#pragma unroll
+    for (int v = 0; v < NB; v++) {
+#pragma unroll
+        for (int h = 0; h < 3; h++) fscr[lane * 3 + h] = sb[(h * NB + v) * nthr + tid];
+        __syncwarp();
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < 7; k++)
+            if (k < cnt) s += fscr[(desc >> (8 * k)) & 0xffu];
+        const double t1 = __shfl_down_sync(0xffffffffu, s, 1), t2 = __shfl_down_sync(0xffffffffu, s, 2);
+        const double t3 = __shfl_down_sync(0xffffffffu, s, 3), t4 = __shfl_down_sync(0xffffffffu, s, 4);
+        const double tot = (((s + t1) + t2) + t3) + t4;
+        __syncwarp();
+        if (lane < 30 && lane % 5 == 0) fscr[96 + lane / 5] = tot;
+        __syncwarp();
+        const int d = lane - L0;
+        if (d >= 0 && d < 12 && !(d & 1)) acc[v] += fscr[96 + (d >> 1)];
+        __syncwarp();
+    }
+#pragma unroll
+    for (int h = 0; h < 3; h++)
+#pragma unroll
+        for (int v = 0; v < NB; v++) sb[(h * NB + v) * nthr + tid] = 0.0;
+}
+
 // ST: every program block is staged (host-checked S3Args::all_staged): program reads are
 // plain shared-memory loads with 32-bit addressing
 template <int MODE, bool FULL, bool WP, bool ST>
@@ -362,6 +423,7 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
     __shared__ double s_x[32], s_y[32], s_z[32], s_mr[R];
     __shared__ uint8_t s_pext[32 * 32];   // [M5][lane] = pext(lane, M5)
     __shared__ uint8_t s_pextw[16 * 16];  // [M4][warp] = pext(warp, M4)
+    __shared__ uint64_t s_fl[64];         // flush entry lists (flush_table3)
 
     const int nW = a.nW, T = 8 + nW, NVU = 9 + nW, nH = a.N - NVU;
     const int tid = threadIdx.x, lane = tid & 31, warp = wuni(tid >> 5);
@@ -373,7 +435,7 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
     double *tileq = reinterpret_cast<double *>(smem_raw);
     double *sb = tileq + 2 * BUFD;                                  // sb[(h * NB + v) * nthreads + tid]
     const int nthr = 32 << nW;
-    double *fscr = sb + (size_t)3 * NB * nthr + (size_t)warp * 32 * 3;
+    double *fscr = sb + (size_t)3 * NB * nthr + (size_t)warp * (32 * 3 + 8);
 
     // tiles of this CTA: a contiguous range of the popcount-sorted visit order, cut by the
     // host so that every CTA gets the same estimated work
@@ -455,6 +517,7 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
             if ((M >> b) & 1u) r |= ((w >> b) & 1u) << j++;
         s_pextw[i] = (uint8_t)r;
     }
+    if ((tid >> 5) == 0) flush_table3(s_fl);
     __syncthreads();   // barriers initialised (thread 0) before any wait
 
     // ---- per-thread constants
@@ -483,32 +546,9 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
     // layer of bin h of this thread at tile popcount K: K + popc_t + beta + 2h.
     auto flush = [&]() {
         if (curK < 0) return;
-        const int betaK = a.c ^ (curK & 1) ^ par_t;
         const int p0 = (a.c ^ curK ^ __popc(warp)) & 1;
-        const int L0 = curK + __popc(warp) + p0;                   // lowest layer of the warp
-        const int z = (popc_t - __popc(warp) + betaK - p0) >> 1;   // this lane's bins sit at L0 + 2 (z + h)
-        const int y = lane;                                        // lanes 0..5: relative layer L0 + 2y
-#pragma unroll
-        for (int v = 0; v < NB; v++) {
-#pragma unroll
-            for (int h = 0; h < 3; h++) fscr[lane * 3 + h] = sb[(h * NB + v) * nthr + tid];
-            __syncwarp();
-            double s = 0.0;
-            for (int l = 0; l < 32; l++) {   // fixed lane order
-                const int hh = y - __shfl_sync(0xffffffffu, z, l);
-                if (y < 6 && hh >= 0 && hh < 3) s += fscr[l * 3 + hh];
-            }
-            __syncwarp();
-#pragma unroll
-            for (int yy = 0; yy < 6; yy++) {
-                const double x = __shfl_sync(0xffffffffu, s, yy);
-                if (lane == L0 + 2 * yy) acc[v] += x;
-            }
-        }
-#pragma unroll
-        for (int h = 0; h < 3; h++)
-#pragma unroll
-            for (int v = 0; v < NB; v++) sb[(h * NB + v) * nthr + tid] = 0.0;
+        const int L0 = curK + __popc(warp) + p0;   // lowest layer of the warp
+        flush_fast3<NB>(s_fl, p0, L0, lane, tid, nthr, sb, fscr, acc);
     };
 
     for (int k = 0; k < nt; k++) {
@@ -1009,6 +1049,7 @@ __global__ void __launch_bounds__(512, 1) k_loop3(const __grid_constant__ S3Args
     __shared__ double s_red[16];
     __shared__ uint8_t s_pext[32 * 32];   // [M5][lane] = pext(lane, M5)
     __shared__ uint8_t s_pextw[16 * 16];  // [M4][warp] = pext(warp, M4)
+    __shared__ uint64_t s_fl[64];         // flush entry lists (flush_table3)
     cg::grid_group grid = cg::this_grid();
 
     const int nW = a.nW, T = 8 + nW, NVU = 9 + nW, nH = a.N - NVU;
@@ -1021,8 +1062,8 @@ __global__ void __launch_bounds__(512, 1) k_loop3(const __grid_constant__ S3Args
     double *tileq = reinterpret_cast<double *>(smem_raw);
     double *sb = tileq + 2 * BUFD;
     const int nthr = 32 << nW;
-    double *fscr = sb + (size_t)3 * 5 * nthr + (size_t)warp * 32 * 3;
-    double *s_blk = sb + (size_t)3 * 5 * nthr + (size_t)nwarps * 32 * 3;
+    double *fscr = sb + (size_t)3 * 5 * nthr + (size_t)warp * (32 * 3 + 8);
+    double *s_blk = sb + (size_t)3 * 5 * nthr + (size_t)nwarps * (32 * 3 + 8);
     double(*s_S)[NV2] = reinterpret_cast<double(*)[NV2]>(s_blk + V2S_TOTAL);
 
     const uint32_t i0 = __ldg(a.range + blockIdx.x), i1 = __ldg(a.range + blockIdx.x + 1);
@@ -1063,6 +1104,7 @@ __global__ void __launch_bounds__(512, 1) k_loop3(const __grid_constant__ S3Args
         L3.kind = active_mask3(1, a.N, a.max_iter) ? K3_SWEEP : K3_FINAL;
     }
     for (int i = tid; i < V2S_TOTAL; i += blockDim.x) s_blk[i] = a.blk[i];
+    if ((tid >> 5) == 0) flush_table3(s_fl);
     if (tid < R)
         s_mr[tid] = ((tid & 1) ? a.nu[1] : 0.0) + ((tid & 2) ? a.nu[7] : 0.0) + ((tid & 4) ? a.nu[8] : 0.0);
     for (int i = tid; i < 32 * 32; i += blockDim.x) {   // pext of lane bits: s_pext[M * 32 + l]
@@ -1132,33 +1174,9 @@ __global__ void __launch_bounds__(512, 1) k_loop3(const __grid_constant__ S3Args
             // layer of bin h of this thread at tile popcount K: K + popc_t + beta + 2h.
             auto flush = [&]() {
                 if (curK < 0) return;
-                const int cc = vld(L3.c);
-                const int betaK = cc ^ (curK & 1) ^ par_t;
-                const int p0 = (cc ^ curK ^ __popc(warp)) & 1;
-                const int L0 = curK + __popc(warp) + p0;                   // lowest layer of the warp
-                const int z = (popc_t - __popc(warp) + betaK - p0) >> 1;   // this lane's bins sit at L0 + 2 (z + h)
-                const int y = lane;                                        // lanes 0..5: relative layer L0 + 2y
-#pragma unroll
-                for (int v = 0; v < NB; v++) {
-#pragma unroll
-                    for (int h = 0; h < 3; h++) fscr[lane * 3 + h] = sb[(h * NB + v) * nthr + tid];
-                    __syncwarp();
-                    double s = 0.0;
-                    for (int l = 0; l < 32; l++) {   // fixed lane order
-                        const int hh = y - __shfl_sync(0xffffffffu, z, l);
-                        if (y < 6 && hh >= 0 && hh < 3) s += fscr[l * 3 + hh];
-                    }
-                    __syncwarp();
-#pragma unroll
-                    for (int yy = 0; yy < 6; yy++) {
-                        const double x = __shfl_sync(0xffffffffu, s, yy);
-                        if (lane == L0 + 2 * yy) acc[v] += x;
-                    }
-                }
-#pragma unroll
-                for (int h = 0; h < 3; h++)
-#pragma unroll
-                    for (int v = 0; v < NB; v++) sb[(h * NB + v) * nthr + tid] = 0.0;
+                const int p0 = (vld(L3.c) ^ curK ^ __popc(warp)) & 1;
+                const int L0 = curK + __popc(warp) + p0;   // lowest layer of the warp
+                flush_fast3<NB>(s_fl, p0, L0, lane, tid, nthr, sb, fscr, acc);
             };
             __syncthreads();   // coefficients written
             for (int k = 0; k < nt; k++) {
@@ -1533,6 +1551,11 @@ __global__ void __launch_bounds__(512, 1) k_loop3(const __grid_constant__ S3Args
 // walked symbolically over the tile's varying units.
 // ---------------------------------------------------------------------------
 constexpr int MAXP = V3_MAXPAIRS;   // distinct (unit, pattern) pairs of one program
+#ifdef HQ_NO_RTAB   // development A/B: no register tables (every register-dependent pair a group)
+constexpr bool RTAB = false;
+#else
+constexpr bool RTAB = true;
+#endif
 constexpr uint32_t PRMASK = 1u | (1u << 1) | (1u << 7) | (1u << 8);   // parity + register units
 
 constexpr int HSLOTS = 2 * MAXP;   // open-addressing index over the keys (load factor <= 1/2)
@@ -1708,7 +1731,7 @@ __device__ int tile_program(const P3Args &a, uint32_t t, double *W0, PairAcc3 &P
                 M |= cond_bits(a, P.key[k] >> 6);
                 k++;
             }
-            if (rm && M == 0u) rtab = true;
+            if (rm && M == 0u && RTAB) rtab = true;
             else nrec += (rm ? 1 : 0) + (((1 << __popc(M)) + 1) >> 1);
         }
         if (rtab) nrec += 8;
@@ -1804,7 +1827,7 @@ __global__ void k_prog_write3(P3Args a, const uint32_t *__restrict__ order, cons
                     k1++;
                 }
                 if (!rm) tab_recs = (uint32_t)(((1 << __popc(M)) + 1) >> 1);
-                else if (M == 0u) rtab = true;
+                else if (M == 0u && RTAB) rtab = true;
                 kend = k1;
             }
             if (rtab) {
@@ -1836,7 +1859,7 @@ __global__ void k_prog_write3(P3Args a, const uint32_t *__restrict__ order, cons
                     M |= cond_bits(a, P.key[k] >> 6);
                     k++;
                 }
-                if (rm && M == 0u) continue;   // in the register table
+                if (rm && M == 0u && RTAB) continue;   // in the register table
                 if (rm && pos == start + tab_recs && rtab) pos += 8;   // skip over the register table
                 // table over the thread bits M: entry idx holds the value of every thread
                 // whose M-bits are pdep(idx, M); a pair applies when its lane / warp units
@@ -1901,12 +1924,11 @@ int choose_nw(int N) {
     return nw;
 }
 
-size_t sweep_smem(int nW, uint32_t maxblk16, int nslots) {
-    (void)nslots;
+size_t sweep_smem(int nW, uint32_t maxblk16) {
     const size_t TS = (size_t)1 << (8 + nW), W = (size_t)1 << nW;
     // tile buffers (q block + program block) x 2, per-thread layer bins (3 x 5 values),
     // per-warp flush scratch
-    return 2 * (TS * 8 + (size_t)maxblk16 * 16) + W * 32 * 3 * 5 * 8 + W * 32 * 3 * 8;
+    return 2 * (TS * 8 + (size_t)maxblk16 * 16) + W * 32 * 3 * 5 * 8 + W * (32 * 3 + 8) * 8;
 }
 
 // CTAs resident per SM the grid is sized for (hq_create: sgrid = nsm * ctas_per_sm)
@@ -1915,20 +1937,22 @@ int ctas_per_sm(int nW) { return std::max(1, 16 >> nW); }
 // dynamic shared memory of k_loop3: the sweep kernel's, then this CTA's scalar block and the
 // phase sums
 size_t loop_smem(int nW, uint32_t maxblk16) {
-    return sweep_smem(nW, maxblk16, 0) + 8 * (size_t)(V2S_TOTAL + HQ_NL * NV2);
+    return sweep_smem(nW, maxblk16) + 8 * (size_t)(V2S_TOTAL + HQ_NL * NV2);
 }
 
 // staged program capacity (records per tile block): as large as fits, at most the largest
-// block (measured: staging every program beats more resident CTAs per SM); sized for the
-// device-resident solve (loop_smem >= sweep_smem)
-uint32_t choose_cap(int nW, uint32_t maxblk16) {
+// block (measured: staging every program beats more resident CTAs per SM); the device-resident
+// solve needs loop_smem - sweep_smem more shared memory
+uint32_t choose_cap(int nW, uint32_t maxblk16, bool dev_loop) {
     const size_t budget = 224u * 1024u - 2048u;
-    const size_t fixed = loop_smem(nW, 0);
+    const size_t fixed = dev_loop ? loop_smem(nW, 0) : sweep_smem(nW, 0);
     if (fixed >= budget) return 0;
     const size_t cap = (budget - fixed) / (2 * 16);
     return (uint32_t)std::min<size_t>(cap, maxblk16);
 }
-int choose_slots(int nW, uint32_t maxblk16) { return sweep_smem(nW, maxblk16, 0) <= 224u * 1024u ? 1 : 0; }
+bool fits_smem(int nW, uint32_t maxblk16, bool dev_loop) {
+    return (dev_loop ? loop_smem(nW, maxblk16) : sweep_smem(nW, maxblk16)) <= 224u * 1024u;
+}
 
 cudaError_t prog_count(const P3Args &a, const uint32_t *order, uint32_t *size16, int *err, int grid, cudaStream_t s) {
     hq3::k_prog_count3<<<grid, 64, 0, s>>>(a, order, size16, err);
@@ -1942,7 +1966,7 @@ cudaError_t prog_write(const P3Args &a, const uint32_t *order, const uint32_t *o
 
 template <int MODE, bool FULL, bool WP, bool ST>
 static cudaError_t launch(const S3Args &a, int grid, cudaStream_t s) {
-    const size_t sm = sweep_smem(a.nW, a.maxblk16, a.nslots);
+    const size_t sm = sweep_smem(a.nW, a.maxblk16);
     auto kern = hq3::k_sweep3<MODE, FULL, WP, ST>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;

@@ -18,7 +18,6 @@
 #include "hq_internal.h"
 
 #define V3_R 8                 // states per thread
-#define V3_MAXSLOTS 8          // CTA ring slots (one tile-sized block each)
 #define V3_HDR16 33            // program header: {info, M, W0} x 32 units, {mu_F, has}
 #define V3_MAXPAIRS 2048
 
@@ -68,7 +67,6 @@ struct S3Args {
     uint32_t total16;
     uint32_t maxblk16;       // largest program block of a CTA tile (16-byte units)
     const uint32_t *range;   // [grid + 1]: CTA b processes visit indices [range[b], range[b+1])
-    int nslots;              // CTA ring slots
     const double *Q;         // neighbour class (read)
     double *P;               // updated class (sweep) / evaluated class (residual)
     const double2 *omkap;    // scatter weights of class c
@@ -128,9 +126,9 @@ cudaError_t sweep(const S3Args &a, int full, int mode, int grid, cudaStream_t s)
 cudaError_t loop(const S3Args &a, int full, int grid, cudaStream_t s);
 int loop_occupancy(const S3Args &a, int full);   // co-resident CTAs per SM (0: does not fit)
 size_t loop_smem(int nW, uint32_t maxblk16);
-size_t sweep_smem(int nW, uint32_t maxblk16, int nslots);
-int choose_slots(int nW, uint32_t maxblk16);
-uint32_t choose_cap(int nW, uint32_t maxblk16);
+size_t sweep_smem(int nW, uint32_t maxblk16);
+bool fits_smem(int nW, uint32_t maxblk16, bool dev_loop);   // the sweep (or device-loop) kernel's smem fits
+uint32_t choose_cap(int nW, uint32_t maxblk16, bool dev_loop);
 int choose_nw(int N);
 int ctas_per_sm(int nW);   // CTAs per SM the sweep grid is sized for
 }  // namespace hq3_launch
