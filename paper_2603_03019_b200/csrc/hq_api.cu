@@ -388,6 +388,9 @@ struct hq_problem {
     int prog_nwv = 0;              // path 3: warp bits varying inside a rate program (nW: CTA programs)
     bool chunked = false;          // path 3: chunked tile order (else popcount order)
     int chunk_bits = 0;            // path 3, chunked order: low tile bits per chunk
+    int h_in = 32;                 // path 3: tile-unit neighbours h < h_in are loaded evict-last
+    int h_out_pol = 0;             // path 3: L2 policy of the other tile-unit neighbour loads
+    int pf_h = 0, pf_o = 0;        // path 3: L2 prefetch distance of the tile-unit slices; of omega/kappa
     std::vector<uint32_t> chunk_range;   // path 3, chunked order: CTA ranges over the visit order
     uint32_t *d_order = nullptr, *d_off16 = nullptr, *d_size16 = nullptr, *d_range = nullptr;
     uint4 *d_prog = nullptr;
@@ -1090,12 +1093,13 @@ static hq_status v3_prepare(hq_problem *h, cudaStream_t s) {
     //  * popcount order (N < 27): tiles by popcount of the tile index; every CTA takes a
     //    contiguous, work-balanced range of it.  A popcount class of q blocks fits in L2 up to
     //    N = 26, so the tile-unit neighbours of the tiles in flight are L2 hits.
-    //  * chunked order (N >= 27): "chunks" = sub-cubes of the b low tile bits (the high tile
-    //    bits fixed); chunk k goes to CTA k mod G, so at any time the CTAs work on G
-    //    consecutive chunks and a neighbour along a high tile bit h was read about 2^h / G
-    //    chunk steps earlier (an L2 hit while that distance stays inside the L2 window); the
-    //    tiles of a chunk follow the popcount of their low bits (b + 1 layer-bin flushes per
-    //    chunk).  Each CTA's chunks are contiguous in `order`, its range is exactly them.
+    //  * group order (N >= 27, the default there): "groups" = sub-cubes of the 11 low tile
+    //    bits, visited in Gray-code order of the high tile bits; the n-th tile of that sequence
+    //    goes to CTA n mod G, so all CTAs work on one group at a time and its q blocks are the
+    //    L2 working set (cfg5: 156 -> 110 B/state of DRAM traffic, -8 % per half-sweep).
+    //  * chunked order (HQ_ORDER=chunk, the default before the group order): "chunks" =
+    //    sub-cubes of the b low tile bits; chunk k goes to CTA k mod G, popcount order of the
+    //    low bits inside a chunk.  Each CTA's chunks are contiguous in `order`.
     std::vector<uint32_t> order;
     order.reserve(ntiles);
     auto popcount_order = [](int bits, std::vector<uint32_t> &out) {
@@ -1111,17 +1115,54 @@ static hq_status v3_prepare(hq_problem *h, cudaStream_t s) {
     };
     h->chunk_bits = 0;
     h->chunked = false;
+    h->h_in = 32;
+    h->h_out_pol = 0;
+    h->pf_h = h->pf_o = 0;
     {
         const char *oenv = getenv("HQ_ORDER");
-        const std::string om = oenv ? oenv : "";
-        bool chunked = N >= 27;
+        // default: group order from N = 27 (measured), popcount order below
+        const std::string om = oenv ? oenv : (N >= 27 ? "group" : "");
+        bool chunked = false;
         if (om == "popcount") chunked = false;
         if (om == "chunk") chunked = true;
         int b = 5;   // measured: cfg4 b = 1 / 3 / 5 -> 2.71 / 2.64 / 2.41 s (popcount order 2.95 s)
         if (const char *benv = getenv("HQ_CHUNK_BITS")) b = atoi(benv);
         b = std::max(0, std::min(b, Nt));
         if (chunked && ((ntiles >> b) < (uint64_t)h->sgrid)) chunked = false;   // too few chunks to spread
-        if (om == "natural") {
+        if (om == "group") {
+            // groups = sub-cubes of the gb low tile bits, visited in Gray-code order of the
+            // high tile bits (consecutive groups are neighbours along one high bit); inside a
+            // group the tiles follow the popcount of their low bits.  The n-th tile of this
+            // group-major sequence goes to CTA n mod G, so all CTAs work on the same group at
+            // the same time: its 2^gb q blocks (and the previous / next group's) are the L2
+            // working set, every neighbour along a low tile bit is an L2 hit.
+            int gb = 11;
+            if (const char *genv = getenv("HQ_GROUP_BITS")) gb = atoi(genv);
+            gb = std::max(0, std::min(gb, Nt));
+            std::vector<uint32_t> low, seq;
+            popcount_order(gb, low);
+            const uint64_t ng = ntiles >> gb;
+            seq.reserve(ntiles);
+            for (uint64_t k = 0; k < ng; k++) {
+                const uint64_t gk = k ^ (k >> 1);
+                for (uint32_t lo : low) seq.push_back((uint32_t)(gk << gb) | lo);
+            }
+            const int G = h->sgrid;
+            h->chunk_bits = gb;
+            h->chunked = true;
+            h->h_in = gb;
+            h->h_out_pol = 2;
+            if (const char *penv = getenv("HQ_HPOL")) h->h_out_pol = atoi(penv);
+            h->pf_h = 4;   // measured at cfg5: 4 units ahead -12 % per half-sweep, 6 ahead -9 %
+            h->pf_o = 1;
+
+            h->chunk_range.assign(G + 1, 0);
+            for (int cta = 0; cta < G; cta++) {
+                h->chunk_range[cta] = (uint32_t)order.size();
+                for (uint64_t n = (uint64_t)cta; n < ntiles; n += (uint64_t)G) order.push_back(seq[n]);
+            }
+            h->chunk_range[G] = (uint32_t)order.size();
+        } else if (om == "natural") {
             // device-resident solve: tiles in natural order, handed out dynamically in units of
             // consecutive tiles, so the CTAs in flight work on neighbouring tiles and the
             // tile-unit neighbours at distance 2^h < L2 window stay L2-resident
@@ -1144,6 +1185,8 @@ static hq_status v3_prepare(hq_problem *h, cudaStream_t s) {
             popcount_order(Nt, order);
         }
     }
+    if (const char *e = getenv("HQ_PFH")) h->pf_h = atoi(e);
+    if (const char *e = getenv("HQ_PFO")) h->pf_o = atoi(e);
     if (dmalloc((void **)&h->d_order, 4 * ntiles) != cudaSuccess ||
         (!h->full_lists && dmalloc((void **)&h->d_lamarr, 8 * S) != cudaSuccess)) {
         cudaGetLastError();
@@ -1220,6 +1263,11 @@ static cudaError_t tiled_sweep(hq_problem *h, const S2Args &sa, int mode, cudaSt
     a.full_lists = sa.full_lists;
     a.warp_programs = (h->prog_nwv == 0) ? 1 : 0;
     a.all_staged = h->maxblk_all <= h->maxrec ? 1 : 0;
+    a.h_in = h->h_in;
+    a.h_out_pol = h->h_out_pol;
+    if (hq3_launch::policies(a.pol) != cudaSuccess) return cudaGetLastError();
+    a.pf_h = h->pf_h;
+    a.pf_o = h->pf_o;
     if (!h->d_wtime && dmalloc((void **)&h->d_wtime, 8 * 4096) == cudaSuccess) cudaMemset(h->d_wtime, 0, 8 * 4096);
     a.wtime = h->d_wtime;
     a.Q = sa.Q;

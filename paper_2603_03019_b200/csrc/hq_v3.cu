@@ -38,6 +38,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <algorithm>
+#include <type_traits>
 #include "hq_internal.h"
 #include "hq_v2.h"
 #include "hq_v3.h"
@@ -132,6 +133,11 @@ __device__ __forceinline__ uint64_t pol_evict_first() {
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
+__device__ __forceinline__ uint64_t pol_evict_normal() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
 __device__ __forceinline__ uint64_t pol_evict_last() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
@@ -159,6 +165,7 @@ __device__ __forceinline__ void prefetch_l2(const void *p, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void prefetch_l1(const void *p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+__device__ __forceinline__ void prefetch_l2line(const void *p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 // rate-program reads: through L1, evicted first from L2 (read once per half-sweep)
 __device__ __forceinline__ double ldp(const double *p, uint64_t pol) {
     double v;
@@ -192,11 +199,15 @@ struct Prog {
 };
 __device__ __forceinline__ double hdr_w0(const uint4 &h) { return __hiloint2double((int)h.w, (int)h.z); }
 
+// neighbour values of the thread's 8 states: a plain array, or 4 x double2 as loaded
+__device__ __forceinline__ double qv(const double (&q)[R], int r) { return q[r]; }
+__device__ __forceinline__ double qv(const double2 (&q)[4], int r) { return (r & 1) ? q[r >> 1].y : q[r >> 1].x; }
+
 // rate of unit u for this thread (w0: the tile-uniform part, already masked by the caller
 // for a lane unit that is free in this lane); register-dependent groups go to A directly
-template <bool WP>
+template <bool WP, class QV>
 __device__ __forceinline__ double unit_rates(const Prog<WP> &P, const uint4 &h, int sh, double w0,
-                                             const double (&q)[R], double (&A)[R]) {
+                                             const QV &q, double (&A)[R]) {
     const uint32_t inf = h.x;
     if (!inf) return w0;
     const uint4 *d = P.pg + V3_HDR16 + ((inf >> 8) & 0x3fffffu);
@@ -211,8 +222,8 @@ __device__ __forceinline__ double unit_rates(const Prog<WP> &P, const uint4 &h, 
 #pragma unroll
         for (int kk = 0; kk < 4; kk++) {
             const double2 w = wr[kk];
-            A[2 * kk] = fma(w.x, q[2 * kk], A[2 * kk]);
-            A[2 * kk + 1] = fma(w.y, q[2 * kk + 1], A[2 * kk + 1]);
+            A[2 * kk] = fma(w.x, qv(q, 2 * kk), A[2 * kk]);
+            A[2 * kk + 1] = fma(w.y, qv(q, 2 * kk + 1), A[2 * kk + 1]);
         }
         d += 8;
     }
@@ -224,9 +235,16 @@ __device__ __forceinline__ double unit_rates(const Prog<WP> &P, const uint4 &h, 
         const double w = reinterpret_cast<const double *>(d + 1)[P.idx(M)];
         d += 1 + (((1 << __popc(M)) + 1) >> 1);
 #pragma unroll
-        for (int r = 0; r < R; r++) pfma(A[r], w, q[r], m8 & (1u << r));
+        for (int r = 0; r < R; r++) pfma(A[r], w, qv(q, r), m8 & (1u << r));
     }
     return Wt;
+}
+
+// the encodings of the three L2 policies (passed to the sweep kernel as parameters)
+__global__ void k_policies(uint64_t *out) {
+    out[0] = pol_evict_last();
+    out[1] = pol_evict_normal();
+    out[2] = pol_evict_first();
 }
 
 // value slots (partial[..][layer][slot]) of the reduced quantities
@@ -420,6 +438,7 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
     constexpr int NB = SL::NB;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t tbar[2];
+    __shared__ unsigned s_done[2];        // HQ_LASTWARP: warps done with the tile in buffer b
     __shared__ double s_x[32], s_y[32], s_z[32], s_mr[R];
     __shared__ uint8_t s_pext[32 * 32];   // [M5][lane] = pext(lane, M5)
     __shared__ uint8_t s_pextw[16 * 16];  // [M4][warp] = pext(warp, M4)
@@ -466,6 +485,7 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
 #endif
     };
     if (tid == 0) {
+        s_done[0] = s_done[1] = 0;
         mbar_init(sptr(&tbar[0]), 1);
         mbar_init(sptr(&tbar[1]), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -531,7 +551,11 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
     const int par_t = popc_t & 1;
     const uint32_t jw = ((uint32_t)warp << 8) | ((uint32_t)lane << 1);   // j_local(r) = jw | (r>>1)<<6 | (r&1)
     const double nu0 = a.nu[0];
-    const uint64_t pol_ef = pol_evict_first(), pol_el = pol_evict_last();
+    // L2 policies: kernel parameters (uniform registers; hq3_launch::policies), so that the
+    // cache-hinted loads need no per-load register-to-uniform moves
+    const uint64_t pol_ef = a.pol[2], pol_el = a.pol[0];
+    const uint64_t pol_out = a.pol[a.h_out_pol];
+    auto hpol = [&](int h) -> uint64_t { return h < a.h_in ? pol_el : pol_out; };
 
     double acc[NB];   // lane L: layer L
 #pragma unroll
@@ -556,41 +580,76 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
         const uint32_t t = __ldg(a.order + tidx);
         const uint32_t jt = t << T;
         const int buf = k & 1;
-        // tile-unit neighbour slices: two units of loads in flight ahead of the one accumulated
-        auto hsrc = [&](int h) -> const double * { return a.Q + ((jt ^ (1u << (T + h))) | jw); };
-        double2 pa[4], pb2[4];
+        // tile-unit neighbour slices: three rotating buffers, each consumed in place and then
+        // refilled three units ahead (the first two are in flight during the in-tile units)
+        const uint32_t jb = jt | jw;
+        auto hsrc = [&](int h) -> const double * { return a.Q + (jb ^ (1u << (T + h))); };
+        double2 hb0[4], hb1[4];
+#ifdef HQ_HBUF3
+        double2 hb2[4];
+#endif
         if (nH > 0) {
 #pragma unroll
-            for (int kk = 0; kk < 4; kk++) pa[kk] = ldg2(hsrc(0) + (kk << 6), pol_el);
+            for (int kk = 0; kk < 4; kk++) hb0[kk] = ldg2(hsrc(0) + (kk << 6), hpol(0));
         }
         if (nH > 1) {
 #pragma unroll
-            for (int kk = 0; kk < 4; kk++) pb2[kk] = ldg2(hsrc(1) + (kk << 6), pol_el);
+            for (int kk = 0; kk < 4; kk++) hb1[kk] = ldg2(hsrc(1) + (kk << 6), hpol(1));
         }
         mbar_wait(sptr(&tbar[buf]), (unsigned)((k >> 1) & 1));
+#ifdef HQ_LASTWARP
+        // no CTA barrier: each warp reports that it is done with tile k-1 (buffer buf ^ 1);
+        // the last one refills that buffer with tile k + 1 (the other warps go on with tile k)
+        if (k == 0) {
+            if (tid == 0 && nt > 1) load_tile(1);
+        } else {
+            __syncwarp();
+            if (lane == 0) {
+                const unsigned old = atom_add_acqrel(sptr(&s_done[buf ^ 1]), 1u);
+                if (old == nwarps - 1) {
+                    s_done[buf ^ 1] = 0;
+                    if (k + 1 < nt) {
+                        fence_proxy_async();
+                        load_tile(k + 1);
+                    }
+                }
+            }
+        }
+#else
         __syncthreads();   // every warp is done with tile k-1: its buffer may be refilled
         if (tid == 0 && k + 1 < nt) {
             fence_proxy_async();
             load_tile(k + 1);
         }
+#endif
 #ifdef HQ_WARP_TIMING
         const long long tw0 = clock64();
 #endif
         const double *tq = tileq + (size_t)buf * BUFD;
-        Prog<WP> P;
+        uint32_t o0, ow;
+        bool staged;
         {
             const uint64_t widx = (uint64_t)tidx << nW;
-            const uint32_t o0 = __ldg(a.off16 + widx), ow = __ldg(a.off16 + widx + warp);
+            o0 = __ldg(a.off16 + widx);
+            ow = __ldg(a.off16 + widx + warp);
             const uint32_t nrec = (widx + nwarps < nwt ? __ldg(a.off16 + widx + nwarps) : a.total16) - o0;
-            P.pg = (ST || nrec <= a.maxblk16) ? reinterpret_cast<const uint4 *>(tq + TS) + (ow - o0) : a.prog + ow;
-            P.pl = s_pext + lane;
-            P.pw = s_pextw + warp;
+            staged = ST || nrec <= a.maxblk16;
         }
         const int K = __popc(t);
         if (K != curK) {
             flush();
             curK = K;
         }
+        // the tile body, instantiated for a program block staged in shared memory (the common
+        // case: shared-memory loads) and for one left in global memory (tile-uniform branch)
+        auto body = [&](auto stag) {
+        constexpr int SM = decltype(stag)::value;   // 1 shared, 0 global, 2 either (generic)
+        Prog<WP> P;
+        P.pg = SM == 1 ? reinterpret_cast<const uint4 *>(tq + TS) + (ow - o0)
+             : SM == 0 ? a.prog + ow
+                       : (staged ? reinterpret_cast<const uint4 *>(tq + TS) + (ow - o0) : a.prog + ow);
+        P.pl = s_pext + lane;
+        P.pw = s_pextw + warp;
         const int beta = a.c ^ (K & 1) ^ par_t;
         const int sh = beta ? 8 : 0;
         const double mu_F = reinterpret_cast<const double *>(P.pg + 32)[0];
@@ -678,35 +737,79 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
                 for (int r = 0; r < R; r++) D[r] = fma(nuu, q[r], D[r]);
             }
         }
-        // ---- tile units (H): neighbour tile slices straight from global memory (L2), two
-        //      units of loads in flight; unrolled by two so the buffers alternate in place
-        auto unit_H = [&](int h, double2 (&buf)[4]) {
+#ifndef HQ_HBUF3
+        // ---- tile units (H): two buffers, copied out before the refill two units ahead
+        auto unit_H = [&](int h, double2 (&hb)[4]) {
             const int u = NVU + h;
+            // L2 prefetch of this warp's 2 KB slice of the neighbour block pf_h units ahead
+            // (16 lanes, one 128-byte line each)
+            if (a.pf_h && h + a.pf_h < nH && lane < 16)
+                prefetch_l2line(a.Q + ((jt ^ (1u << (T + h + a.pf_h))) | ((uint32_t)warp << 8)) + lane * 16);
+            double2 qq[4];
 #pragma unroll
-            for (int kk = 0; kk < 4; kk++) {
-                q[2 * kk] = buf[kk].x;
-                q[2 * kk + 1] = buf[kk].y;
-            }
+            for (int kk = 0; kk < 4; kk++) qq[kk] = hb[kk];
             if (h + 2 < nH) {
                 const double *src = hsrc(h + 2);
+                const uint64_t pl2 = hpol(h + 2);
 #pragma unroll
-                for (int kk = 0; kk < 4; kk++) buf[kk] = ldg2(src + (kk << 6), pol_el);
+                for (int kk = 0; kk < 4; kk++) hb[kk] = ldg2(src + (kk << 6), pl2);
             }
             if ((t >> h) & 1u) {
                 const uint4 hu = P.hdr(u);
-                const double Wt = unit_rates(P, hu, sh, hdr_w0(hu), q, A);
+                const double Wt = unit_rates(P, hu, sh, hdr_w0(hu), qq, A);
 #pragma unroll
-                for (int r = 0; r < R; r++) A[r] = fma(Wt, q[r], A[r]);
+                for (int r = 0; r < R; r++) A[r] = fma(Wt, qv(qq, r), A[r]);
             } else {
                 const double nuu = a.nu[u];
 #pragma unroll
-                for (int r = 0; r < R; r++) D[r] = fma(nuu, q[r], D[r]);
+                for (int r = 0; r < R; r++) D[r] = fma(nuu, qv(qq, r), D[r]);
             }
         };
+        if (MODE < 2 && a.pf_o)   // this warp's 4 KB of scatter weights, needed in the epilogue
+            prefetch_l2line(a.omkap + (jt | ((uint32_t)warp << 8)) + lane * 8);
         for (int h = 0; h < nH; h += 2) {
-            unit_H(h, pa);
-            if (h + 1 < nH) unit_H(h + 1, pb2);
+            unit_H(h, hb0);
+            if (h + 1 < nH) unit_H(h + 1, hb1);
         }
+#else
+        // ---- tile units (H): neighbour tile slices straight from global memory (L2)
+        auto unit_H = [&](int h, double2 (&hb)[4]) {
+            const int u = NVU + h;
+            // L2 prefetch of this warp's 2 KB slice of the neighbour block pf_h units ahead
+            // (16 lanes, one 128-byte line each)
+            if (a.pf_h && h + a.pf_h < nH && lane < 16)
+                prefetch_l2line(a.Q + ((jt ^ (1u << (T + h + a.pf_h))) | ((uint32_t)warp << 8)) + lane * 16);
+            if ((t >> h) & 1u) {
+                const uint4 hu = P.hdr(u);
+                const double Wt = unit_rates(P, hu, sh, hdr_w0(hu), hb, A);
+#pragma unroll
+                for (int r = 0; r < R; r++) A[r] = fma(Wt, qv(hb, r), A[r]);
+            } else {
+                const double nuu = a.nu[u];
+#pragma unroll
+                for (int r = 0; r < R; r++) D[r] = fma(nuu, qv(hb, r), D[r]);
+            }
+            if (h + 3 < nH) {
+                const double *src = hsrc(h + 3);
+                const uint64_t pl3 = hpol(h + 3);
+#pragma unroll
+                for (int kk = 0; kk < 4; kk++) hb[kk] = ldg2(src + (kk << 6), pl3);
+            }
+        };
+        if (MODE < 2 && a.pf_o)   // this warp's 4 KB of scatter weights, needed in the epilogue
+            prefetch_l2line(a.omkap + (jt | ((uint32_t)warp << 8)) + lane * 8);
+        if (nH > 2) {
+            const double *src = hsrc(2);
+            const uint64_t pl2 = hpol(2);
+#pragma unroll
+            for (int kk = 0; kk < 4; kk++) hb2[kk] = ldg2(src + (kk << 6), pl2);
+        }
+        for (int h = 0; h < nH; h += 3) {
+            unit_H(h, hb0);
+            if (h + 1 < nH) unit_H(h + 1, hb1);
+            if (h + 2 < nH) unit_H(h + 2, hb2);
+        }
+#endif
         // ---- lambda_m: Lambda minus the atoms whose whole (truncated) list is busy
         double lam[R];
         if (FULL) {
@@ -802,6 +905,13 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
                 }
             }
         }
+        };
+#ifdef HQ_NO_SPLIT
+        body(std::integral_constant<int, 2>{});
+#else
+        if (ST || staged) body(std::integral_constant<int, 1>{});
+        else body(std::integral_constant<int, 0>{});
+#endif
     }
     flush();
 #ifdef HQ_WARP_TIMING
@@ -1993,6 +2103,21 @@ static cudaError_t sweep_st(const S3Args &a, int full, int mode, int grid, cudaS
 template <bool WP>
 static cudaError_t sweep_wp(const S3Args &a, int full, int mode, int grid, cudaStream_t s) {
     return a.all_staged ? sweep_st<WP, true>(a, full, mode, grid, s) : sweep_st<WP, false>(a, full, mode, grid, s);
+}
+
+cudaError_t policies(uint64_t *host3) {
+    static uint64_t cache[3] = {0, 0, 0};
+    if (!cache[0]) {
+        uint64_t *d = nullptr;
+        cudaError_t e = cudaMalloc((void **)&d, 3 * sizeof(uint64_t));
+        if (e != cudaSuccess) return e;
+        hq3::k_policies<<<1, 1>>>(d);
+        e = cudaMemcpy(cache, d, sizeof(cache), cudaMemcpyDeviceToHost);
+        cudaFree(d);
+        if (e != cudaSuccess) return e;
+    }
+    for (int i = 0; i < 3; i++) host3[i] = cache[i];
+    return cudaSuccess;
 }
 
 cudaError_t sweep(const S3Args &a, int full, int mode, int grid, cudaStream_t s) {
