@@ -391,6 +391,8 @@ struct hq_problem {
     int h_in = 32;                 // path 3: tile-unit neighbours h < h_in are loaded evict-last
     int h_out_pol = 0;             // path 3: L2 policy of the other tile-unit neighbour loads
     int pf_h = 0, pf_o = 0;        // path 3: L2 prefetch distance of the tile-unit slices; of omega/kappa
+    int in_pol = 0;                // path 3: L2 policy of the q blocks and in-group neighbours (S3Args::pol)
+    int pf_min = 0;                // path 3: prefetch only the tile units h >= pf_min
     std::vector<uint32_t> chunk_range;   // path 3, chunked order: CTA ranges over the visit order
     uint32_t *d_order = nullptr, *d_off16 = nullptr, *d_size16 = nullptr, *d_range = nullptr;
     uint4 *d_prog = nullptr;
@@ -1187,6 +1189,10 @@ static hq_status v3_prepare(hq_problem *h, cudaStream_t s) {
     }
     if (const char *e = getenv("HQ_PFH")) h->pf_h = atoi(e);
     if (const char *e = getenv("HQ_PFO")) h->pf_o = atoi(e);
+    h->in_pol = 0;
+    if (const char *e = getenv("HQ_INPOL")) h->in_pol = atoi(e);
+    h->pf_min = 0;
+    if (const char *e = getenv("HQ_PFMIN")) h->pf_min = atoi(e);
     if (dmalloc((void **)&h->d_order, 4 * ntiles) != cudaSuccess ||
         (!h->full_lists && dmalloc((void **)&h->d_lamarr, 8 * S) != cudaSuccess)) {
         cudaGetLastError();
@@ -1267,6 +1273,8 @@ static cudaError_t tiled_sweep(hq_problem *h, const S2Args &sa, int mode, cudaSt
     a.h_out_pol = h->h_out_pol;
     if (hq3_launch::policies(a.pol) != cudaSuccess) return cudaGetLastError();
     a.pf_h = h->pf_h;
+    a.in_pol = h->in_pol;
+    a.pf_min = h->pf_min;
     a.pf_o = h->pf_o;
     if (!h->d_wtime && dmalloc((void **)&h->d_wtime, 8 * 4096) == cudaSuccess) cudaMemset(h->d_wtime, 0, 8 * 4096);
     a.wtime = h->d_wtime;

@@ -245,6 +245,9 @@ __global__ void k_policies(uint64_t *out) {
     out[0] = pol_evict_last();
     out[1] = pol_evict_normal();
     out[2] = pol_evict_first();
+    uint64_t p;   // evict-last for half of the lines (address-hashed), the rest unchanged
+    asm volatile("createpolicy.fractional.L2::evict_last.L2::evict_unchanged.b64 %0, 0.5;" : "=l"(p));
+    out[3] = p;
 }
 
 // value slots (partial[..][layer][slot]) of the reduced quantities
@@ -474,7 +477,7 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
         double *b = tileq + (size_t)buf * BUFD;
         mbar_expect(bar, TS * 8u + (staged ? nrec * 16u : 0u));
 #ifndef HQ_NO_L2POL
-        bulk_g2s_pol(sptr(b), a.Q + ((size_t)t << T), TS * 8u, bar, pol_evict_last());
+        bulk_g2s_pol(sptr(b), a.Q + ((size_t)t << T), TS * 8u, bar, a.pol[a.in_pol]);
 #else
         bulk_g2s(sptr(b), a.Q + ((size_t)t << T), TS * 8u, bar);
 #endif
@@ -553,7 +556,7 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
     const double nu0 = a.nu[0];
     // L2 policies: kernel parameters (uniform registers; hq3_launch::policies), so that the
     // cache-hinted loads need no per-load register-to-uniform moves
-    const uint64_t pol_ef = a.pol[2], pol_el = a.pol[0];
+    const uint64_t pol_ef = a.pol[2], pol_el = a.pol[a.in_pol];
     const uint64_t pol_out = a.pol[a.h_out_pol];
     auto hpol = [&](int h) -> uint64_t { return h < a.h_in ? pol_el : pol_out; };
 
@@ -743,7 +746,7 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
             const int u = NVU + h;
             // L2 prefetch of this warp's 2 KB slice of the neighbour block pf_h units ahead
             // (16 lanes, one 128-byte line each)
-            if (a.pf_h && h + a.pf_h < nH && lane < 16)
+            if (a.pf_h && h + a.pf_h < nH && h + a.pf_h >= a.pf_min && lane < 16)
                 prefetch_l2line(a.Q + ((jt ^ (1u << (T + h + a.pf_h))) | ((uint32_t)warp << 8)) + lane * 16);
             double2 qq[4];
 #pragma unroll
@@ -777,7 +780,7 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
             const int u = NVU + h;
             // L2 prefetch of this warp's 2 KB slice of the neighbour block pf_h units ahead
             // (16 lanes, one 128-byte line each)
-            if (a.pf_h && h + a.pf_h < nH && lane < 16)
+            if (a.pf_h && h + a.pf_h < nH && h + a.pf_h >= a.pf_min && lane < 16)
                 prefetch_l2line(a.Q + ((jt ^ (1u << (T + h + a.pf_h))) | ((uint32_t)warp << 8)) + lane * 16);
             if ((t >> h) & 1u) {
                 const uint4 hu = P.hdr(u);
@@ -2106,17 +2109,17 @@ static cudaError_t sweep_wp(const S3Args &a, int full, int mode, int grid, cudaS
 }
 
 cudaError_t policies(uint64_t *host3) {
-    static uint64_t cache[3] = {0, 0, 0};
+    static uint64_t cache[4] = {0, 0, 0, 0};
     if (!cache[0]) {
         uint64_t *d = nullptr;
-        cudaError_t e = cudaMalloc((void **)&d, 3 * sizeof(uint64_t));
+        cudaError_t e = cudaMalloc((void **)&d, 4 * sizeof(uint64_t));
         if (e != cudaSuccess) return e;
         hq3::k_policies<<<1, 1>>>(d);
         e = cudaMemcpy(cache, d, sizeof(cache), cudaMemcpyDeviceToHost);
         cudaFree(d);
         if (e != cudaSuccess) return e;
     }
-    for (int i = 0; i < 3; i++) host3[i] = cache[i];
+    for (int i = 0; i < 4; i++) host3[i] = cache[i];
     return cudaSuccess;
 }
 

@@ -80,9 +80,11 @@ struct S3Args {
     // group order) evict-last; the others h_out_pol (0 evict-last, 1 evict-normal, 2 evict-first)
     int h_in;
     int h_out_pol;
-    uint64_t pol[3];         // L2 policy encodings: evict-last, evict-normal, evict-first (k_sweep3)
+    uint64_t pol[4];         // L2 policy encodings: evict-last, evict-normal, evict-first, half evict-last
+    int in_pol;              // policy (index into pol) of the q blocks and the neighbours h < h_in
     int pf_h;                // > 0: L2 prefetch of the tile-unit neighbour slices pf_h units ahead
     int pf_o;                // 1: L2 prefetch of the tile's scatter weights before the tile units
+    int pf_min;              // prefetch only the tile units h >= pf_min
     // folded scalar step (MODE 0/1): every CTA first performs the scalar step of the previous
     // half-sweep (class prev_c, layers prev_active) from that launch's transposed partials
     // prev_partial and the block coef; CTA 0 stores the updated block in blk_out
@@ -128,7 +130,7 @@ cudaError_t prog_count(const P3Args &a, const uint32_t *order, uint32_t *size16,
 cudaError_t prog_write(const P3Args &a, const uint32_t *order, const uint32_t *off16, uint4 *prog, int *err,
                        int grid, cudaStream_t s);
 cudaError_t sweep(const S3Args &a, int full, int mode, int grid, cudaStream_t s);
-cudaError_t policies(uint64_t *host3);   // the L2 policy encodings (S3Args::pol), cached per process
+cudaError_t policies(uint64_t *host4);   // the L2 policy encodings (S3Args::pol), cached per process
 // device-resident solve (k_loop3): one cooperative launch runs every half-sweep, the
 // convergence checks and the verification residual; grid = the CTA ranges (a.range)
 cudaError_t loop(const S3Args &a, int full, int grid, cudaStream_t s);

@@ -8,8 +8,9 @@ the CUDA result is checked against:
   * cfg4 (N = 28, truncated lists) and cfg5 (N = 31): the oracle's own
     balance equation (Eq. balance_eq_heter) evaluated state by
     state at seeded samples of the GPU pi, plus properties that hold at any
-    size: sum pi = 1, pi >= 0, layer-cut balance, sum rho_ij = 1 and the unit
-    flow identity nu_i rho_i = Lambda (1 - loss) sum_j rho_ij;
+    size: sum pi = 1, pi >= 0, the loss ordering (truncated lists: loss > P(all busy)),
+    sum rho_ij = 1 and the unit flow identity nu_i rho_i = Lambda (1 - loss) sum_j rho_ij;
+    (the whole-vector checks at these sizes are in test_gpu_fullsize.py);
   * N = 31 ordered hunt: the Erlang-B closed forms for the layer masses, the
     per-unit workloads and the loss (textbook, independent of the method).
 """

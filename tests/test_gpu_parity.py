@@ -109,7 +109,9 @@ def test_dense_lu_tiny(hq):
             assert abs(g["loss"] - loss) <= 1e-13
 
 
-def test_single_atom_and_homogeneous_erlang(hq):
+def test_cfg2_homogeneous_copy_erlang_layer_masses(hq):
+    """Homogeneous copy of cfg2 (nu_i = 1, reading C10): the layer masses are the truncated
+    Poisson (Erlang loss) distribution, whatever the preference lists."""
     from test_oracle_pins import truncated_poisson, layer_mass
 
     inst = hqinst.homogeneous_copy(hqinst.config_instance(2))
