@@ -247,7 +247,7 @@ const char *hq_error_string(hq_handle h);
  *   [8] time in the sweep kernels in ms (CUDA events), [9] sweep-kernel
  *   launches, [10] residual-kernel time in ms, [11] one-off per-instance
  *   precompute time in ms (rate programs, scatter weights), [12] bytes of
- *   rate programs, [13] code path (1: N < 8 two-pass, 2: warp-tiled, 3: CTA-tiled),
+ *   rate programs, [13] code path (1: N < 9 two-pass or the fallback, 3: CTA-tiled),
  *   [14] largest rate-program block of a CTA tile (16-byte records),
  *   [15] warp bits varying inside a rate program (0: one program per warp tile,
  *        the default; nW: one program per CTA tile, HQ_PROG=cta),

@@ -198,80 +198,6 @@ double binom(int n, int k) {
     return std::floor(r + 0.5);
 }
 
-// Internal unit order for the tile programs: units 0..7 vary inside a warp
-// tile, so they should be the units that least often precede other units in
-// the preference lists (fewest trie nodes with the unit on the path above
-// them): this minimises the per-state rate pairs.  perm[internal] = ABI unit.
-std::vector<int> choose_perm(int N, const TrieHost &tr) {
-    std::vector<int> perm(N);
-    for (int u = 0; u < N; u++) perm[u] = u;
-    const char *env = getenv("HQ_PERM");
-    if (N < 8 || (env && std::string(env) == "identity")) return perm;
-    // prefix counts: trie nodes with the unit strictly above them on the path
-    std::vector<long> cnt(N, 0);
-    std::vector<int> stk;
-    std::vector<uint32_t> path(tr.node.size()), pre(tr.node.size());
-    std::vector<uint32_t> pstk;
-    for (size_t v = 0; v < tr.node.size(); v++) {
-        const int u = tr.node[v].x & 0xff, d = (tr.node[v].x >> 8) & 0xff;
-        stk.resize(d - 1);
-        pstk.resize(d - 1);
-        for (int a : stk) cnt[a]++;
-        pre[v] = d >= 2 ? pstk[d - 2] : 0u;
-        path[v] = pre[v] | (1u << u);
-        stk.push_back(u);
-        pstk.push_back(path[v]);
-    }
-    std::vector<int> idx(N);
-    for (int u = 0; u < N; u++) idx[u] = u;
-    std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return cnt[a] < cnt[b]; });
-    std::vector<int> L8(idx.begin(), idx.begin() + 8);
-    uint32_t vmask = 0;
-    for (int x : L8) vmask |= 1u << x;
-    // Expected per-state cost of the rate pairs over uniformly random tiles for
-    // a choice of the three register-state units T (internal 0, 6, 7): a node
-    // survives with probability 2^-(fixed units on its path); it costs a
-    // lane-only pair (~1.25 instr/state) or a register-state pair (~4.5).
-    double best = 1e300;
-    int bt[3] = {L8[0], L8[1], L8[2]};
-    for (int a1 = 0; a1 < 8; a1++)
-        for (int a2 = a1 + 1; a2 < 8; a2++)
-            for (int a3 = a2 + 1; a3 < 8; a3++) {
-                const uint32_t T = (1u << L8[a1]) | (1u << L8[a2]) | (1u << L8[a3]);
-                const uint32_t lanes = vmask & ~T;
-                double cost = 0.0;
-                for (size_t v = 0; v < tr.node.size(); v++) {
-                    const int u = tr.node[v].x & 0xff;
-                    const int f = __builtin_popcount(path[v] & ~vmask);
-                    const double w = std::ldexp(1.0, -f);
-                    uint32_t S = pre[v] & vmask;
-                    if ((lanes >> u) & 1u) S |= 1u << u;
-                    if (!S) continue;
-                    cost += (S & T) ? 4.5 * w : 1.25 * w;
-                }
-                if (cost < best) {
-                    best = cost;
-                    bt[0] = L8[a1];
-                    bt[1] = L8[a2];
-                    bt[2] = L8[a3];
-                }
-            }
-    std::vector<char> used(N, 0);
-    perm[0] = bt[0];
-    perm[6] = bt[1];
-    perm[7] = bt[2];
-    for (int q = 0; q < 3; q++) used[bt[q]] = 1;
-    int k = 1;
-    for (int x : L8)
-        if (!used[x]) {
-            perm[k++] = x;
-            used[x] = 1;
-        }
-    k = 8;
-    for (int u = 0; u < N; u++)
-        if (!used[u]) perm[k++] = u;
-    return perm;
-}
 
 
 // Internal unit order for the CTA-tiled path (hq_v3.h).  Rate programs are per warp
@@ -381,7 +307,7 @@ struct hq_problem {
     int grid = 0;
     // v2 (N >= 8) device state
     bool v2 = false, v2_ready = false;
-    int path = 1;                  // 1: N < 8 two-pass, 2: warp-tiled (hq_v2.cu), 3: CTA-tiled (hq_v3.cu)
+    int path = 1;                  // 1: N < 9 two-pass (hq_kernels.cu), 3: CTA-tiled (hq_v3.cu)
     int nW = 0;                    // path 3: log2(warps per CTA)
     uint32_t maxblk_all = 0;       // path 3: largest program block of a CTA tile (records)
     unsigned long long *d_wtime = nullptr;   // path 3: per-warp busy cycles (-DHQ_WARP_TIMING builds)
@@ -535,15 +461,16 @@ extern "C" hq_status hq_create(int N, int J, const double *lambda, const double 
     h->pref.assign(pref, pref + (size_t)J * N);
     {
         TrieHost abi = build_trie(N, J, lambda, pref);
-        const char *penv = getenv("HQ_PATH");
-        h->path = N < 8 ? 1 : (N < 9 || (penv && std::string(penv) == "2")) ? 2 : 3;
+        // N < 9: the two-pass kernels (per-thread trie walk); N >= 9: the CTA-tiled path
+        h->path = N < 9 ? 1 : 3;
         if (h->path == 3) {
             h->nW = hq3_launch::choose_nw(N);
             if (const char *wenv = getenv("HQ_NW"))   // development override (log2 warps per CTA)
                 h->nW = std::max(0, std::min({atoi(wenv), 4, N - 9}));
             h->perm = choose_perm_v3(N, abi, h->nW);
-        } else {
-            h->perm = choose_perm(N, abi);
+        } else {   // the two-pass path works in ABI unit order
+            h->perm.resize(N);
+            for (int u = 0; u < N; u++) h->perm[u] = u;
         }
         std::vector<int> inv(N);
         for (int u = 0; u < N; u++) inv[h->perm[u]] = u;
@@ -553,7 +480,7 @@ extern "C" hq_status hq_create(int N, int J, const double *lambda, const double 
         h->nu_int.resize(N);
         for (int u = 0; u < N; u++) h->nu_int[u] = mu[h->perm[u]];
     }
-    h->v2 = N >= 8;
+    h->v2 = h->path == 3;   // the tiled path (a-priori normalisation, one pass per half-sweep)
     // device-resident solve by default where it is the faster path (measured, DESIGN.md §9:
     // N = 18 14.3 vs 16.2 ms; N = 24 145 vs 123 ms); HQ_LOOP=device|host overrides
     h->dev_loop = N < 21;
@@ -696,172 +623,6 @@ static hq_status true_residual(hq_problem *h, cudaStream_t s, double *res, int *
     return HQ_OK;
 }
 
-
-// ---------------------------------------------------------------------------
-// v2 path (N >= 8): precompute once per handle, then one kernel per half-sweep.
-// ---------------------------------------------------------------------------
-static hq_status v2_prepare(hq_problem *h, cudaStream_t s) {
-    if (h->v2_ready) return HQ_OK;
-    const int N = h->N;
-    const uint64_t S = 1ull << N, half = S >> 1;
-    const int Nt = h->path == 3 ? N - 9 - h->nW : N - 8;
-    const uint64_t ntiles = 1ull << Nt;
-    // tile visit order: by popcount of the tile index, ascending within a popcount class
-    std::vector<uint32_t> order;
-    order.reserve(ntiles);
-    for (int K = 0; K <= Nt; K++) {
-        if (K == 0) {
-            order.push_back(0);
-            continue;
-        }
-        uint64_t x = (1ull << K) - 1;
-        while (x < ntiles) {
-            order.push_back((uint32_t)x);
-            const uint64_t cc = x & (~x + 1), r = x + cc;
-            x = (((r ^ x) >> 2) / cc) | r;
-        }
-    }
-    // path 3: one rate program per CTA tile
-    const int nWp = 0;
-    const uint64_t nprog = ntiles << nWp;
-    if (nWp) {
-        std::vector<uint32_t> w(nprog);
-        for (uint64_t i = 0; i < ntiles; i++)
-            for (uint32_t x = 0; x < (1u << nWp); x++) w[(i << nWp) | x] = (order[i] << nWp) | x;
-        order.swap(w);
-    }
-    auto alloc = [&](void **p, size_t bytes) -> cudaError_t { return dmalloc(p, bytes ? bytes : 16); };
-    if (alloc((void **)&h->d_order, 4 * nprog) != cudaSuccess || alloc((void **)&h->d_off16, 4 * nprog) != cudaSuccess ||
-        alloc((void **)&h->d_size16, 4 * nprog) != cudaSuccess ||
-        (!h->full_lists && alloc((void **)&h->d_lamarr, 8 * S) != cudaSuccess)) {
-        cudaGetLastError();
-        h->err = "device memory for the tile tables could not be allocated";
-        return HQ_E_NOMEM;
-    }
-    HQ_CUDA(cudaMemcpyAsync(h->d_order, order.data(), 4 * nprog, cudaMemcpyHostToDevice, s));
-    P2Args pa;
-    memset(&pa, 0, sizeof(pa));
-    pa.N = N;
-    pa.full_lists = h->full_lists ? 1 : 0;
-    pa.ntiles = ntiles;
-    pa.Lam = h->Lam;
-    for (int u = 0; u < 32; u++) pa.nu[u] = u < N ? h->nu_int[u] : 0.0;
-    pa.nnodes = (int)h->trie.node.size();
-    pa.node = h->d_node;
-    pa.lam_thr = h->d_lthr;
-    pa.lam_end = h->d_lend;
-    cudaEvent_t e0 = h->event(0), e1 = h->event(1);
-    HQ_CUDA(cudaEventRecord(e0, s));
-    const int g = h->nsm * 8;
-    if (!h->full_lists) HQ_CUDA(hq2_launch::lambda_states(pa, h->d_lamarr, g, s));
-    HQ_CUDA(hq2_launch::omkap(pa, h->d_lamarr, h->d_omkap, g, s));
-    HQ_CUDA(cudaMemsetAsync(h->d_err, 0, sizeof(int), s));
-    P3Args p3;
-    memset(&p3, 0, sizeof(p3));
-    p3.N = N;
-    p3.nW = h->nW;
-    p3.full_lists = pa.full_lists;
-    p3.ntiles = nprog;
-    for (int u = 0; u < 32; u++) p3.nu[u] = pa.nu[u];
-    p3.nnodes = pa.nnodes;
-    p3.node = pa.node;
-    p3.lam_thr = pa.lam_thr;
-    p3.lam_end = pa.lam_end;
-    if (h->path == 3) HQ_CUDA(hq3_launch::prog_count(p3, h->d_order, h->d_size16, h->d_err, g, s));
-    else HQ_CUDA(hq2_launch::prog_count(pa, h->d_order, h->d_size16, h->d_err, g, s));
-    size_t tmpb = 0;
-    HQ_CUDA(hq2_launch::prog_scan(h->d_size16, h->d_off16, nprog, nullptr, &tmpb, s));
-    void *tmp = nullptr;
-    HQ_CUDA(alloc(&tmp, tmpb));
-    HQ_CUDA(hq2_launch::prog_scan(h->d_size16, h->d_off16, nprog, tmp, &tmpb, s));
-    uint32_t *d_max = nullptr;
-    HQ_CUDA(alloc((void **)&d_max, 4));
-    size_t tmpb2 = 0;
-    HQ_CUDA(hq2_launch::prog_max(h->d_size16, d_max, nprog, nullptr, &tmpb2, s));
-    void *tmp2 = nullptr;
-    HQ_CUDA(alloc(&tmp2, tmpb2));
-    HQ_CUDA(hq2_launch::prog_max(h->d_size16, d_max, nprog, tmp2, &tmpb2, s));
-    uint32_t last[2] = {0, 0};
-    int herr = 0;
-    HQ_CUDA(cudaMemcpyAsync(&h->maxrec, d_max, 4, cudaMemcpyDeviceToHost, s));
-    HQ_CUDA(cudaMemcpyAsync(&last[0], h->d_off16 + nprog - 1, 4, cudaMemcpyDeviceToHost, s));
-    HQ_CUDA(cudaMemcpyAsync(&last[1], h->d_size16 + nprog - 1, 4, cudaMemcpyDeviceToHost, s));
-    HQ_CUDA(cudaMemcpyAsync(&herr, h->d_err, sizeof(int), cudaMemcpyDeviceToHost, s));
-    HQ_CUDA(cudaStreamSynchronize(s));
-    if (h->path == 3) {   // program block sizes -> largest block, and work-balanced CTA ranges
-        std::vector<uint32_t> sz(nprog);
-        HQ_CUDA(cudaMemcpy(sz.data(), h->d_size16, 4 * nprog, cudaMemcpyDeviceToHost));
-        uint32_t mb = 0;
-        std::vector<double> cost(ntiles);
-        double tot = 0.0;
-        for (uint64_t i = 0; i < ntiles; i++) {
-            uint32_t b = 0;
-            for (uint32_t x = 0; x < (1u << nWp); x++) b += sz[(i << nWp) | x];
-            mb = std::max(mb, b);
-            // estimated work of a tile in program-record units: the gather of its 2^(8+nW)
-            // states plus the evaluation of each program record by every warp
-            cost[i] = 256.0 + (double)b;
-            tot += cost[i];
-        }
-        h->maxrec = mb;
-        const int G = h->sgrid;
-        std::vector<uint32_t> range(G + 1, (uint32_t)ntiles);
-        range[0] = 0;
-        double acc = 0.0;
-        int b = 1;
-        for (uint64_t i = 0; i < ntiles && b < G; i++) {
-            acc += cost[i];
-            while (b < G && acc >= tot * b / G) range[b++] = (uint32_t)(i + 1);
-        }
-        dfree(h->d_range);
-        h->d_range = nullptr;
-        HQ_CUDA(dmalloc((void **)&h->d_range, 4 * (G + 1)));
-        HQ_CUDA(cudaMemcpy(h->d_range, range.data(), 4 * (G + 1), cudaMemcpyHostToDevice));
-    }
-    dfree(tmp);
-    dfree(tmp2);
-    dfree(d_max);
-    if (h->path == 3) {   // staged program capacity; larger blocks are read from global memory
-        h->maxblk_all = h->maxrec;
-        h->maxrec = hq3_launch::choose_cap(h->nW, h->maxrec, h->dev_loop);
-    }
-    if (h->path == 3 ? !hq3_launch::fits_smem(h->nW, h->maxrec, h->dev_loop) : hq2_launch::sweep_smem(h->maxrec) > 150u * 1024u) {
-        h->err = "rate program of a tile exceeds the shared-memory budget";
-        return HQ_E_NUMERIC;
-    }
-    if (herr) {
-        h->err = "rate program overflow (too many distinct (unit, pattern) pairs in a tile)";
-        return HQ_I_OVERFLOW;
-    }
-    const uint64_t total16 = (uint64_t)last[0] + last[1];
-    h->total16 = (uint32_t)total16;
-    if (alloc((void **)&h->d_prog, 16 * total16) != cudaSuccess) {
-        cudaGetLastError();
-        h->err = "device memory for the rate programs could not be allocated";
-        return HQ_E_NOMEM;
-    }
-    if (h->path == 3) {
-        HQ_CUDA(hq3_launch::prog_write(p3, h->d_order, h->d_off16, h->d_prog, h->d_err, g, s));
-        HQ_CUDA(cudaMemcpyAsync(&herr, h->d_err, sizeof(int), cudaMemcpyDeviceToHost, s));
-        HQ_CUDA(cudaStreamSynchronize(s));
-        if (herr) {
-            h->err = "rate program overflow (more than 255 lane-only pairs or groups for a unit)";
-            return HQ_I_OVERFLOW;
-        }
-    }
-    else HQ_CUDA(hq2_launch::prog_write(pa, h->d_order, h->d_off16, h->d_prog, g, s));
-    HQ_CUDA(cudaEventRecord(e1, s));
-    HQ_CUDA(cudaEventSynchronize(e1));
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, e0, e1);
-    h->precompute_ms = ms;
-    h->prog_bytes = 16.0 * (double)total16;
-    dfree(h->d_size16);
-    h->d_size16 = nullptr;
-    (void)half;
-    h->v2_ready = true;
-    return HQ_OK;
-}
 
 // ---------------------------------------------------------------------------
 // path 3 preparation: rate programs at warp-tile or CTA-tile granularity (hq_v3.h)
@@ -1247,9 +1008,8 @@ static hq_status v3_prepare(hq_problem *h, cudaStream_t s) {
     return HQ_OK;
 }
 
-// one sweep / residual launch of the tiled paths (2: hq_v2.cu, 3: hq_v3.cu)
+// one sweep / residual launch of the tiled path (hq_v3.cu)
 static cudaError_t tiled_sweep(hq_problem *h, const S2Args &sa, int mode, cudaStream_t s, const FoldArgs *f) {
-    if (h->path != 3) return hq2_launch::sweep(sa, mode, h->sgrid, s);
     S3Args a;
     memset(&a, 0, sizeof(a));
     a.N = sa.N;
@@ -1345,7 +1105,7 @@ static hq_status v2_residual(hq_problem *h, cudaStream_t s, S2Args sa, SolveOut 
 }
 
 static hq_status solve_v2(hq_problem *h, double tol, int max_iter, double *pi, cudaStream_t s, SolveOut &o) {
-    hq_status st = h->path == 3 ? v3_prepare(h, s) : v2_prepare(h, s);
+    hq_status st = v3_prepare(h, s);
     if (st != HQ_OK) return st;
     const int N = h->N;
     const uint64_t half = 1ull << (N - 1);

@@ -82,14 +82,9 @@ enum {
 namespace hq2_launch {
 cudaError_t lambda_states(const P2Args &a, double *lamarr, int grid, cudaStream_t s);
 cudaError_t omkap(const P2Args &a, const double *lamarr, double2 *omkap, int grid, cudaStream_t s);
-cudaError_t prog_count(const P2Args &a, const uint32_t *order, uint32_t *size16, int *err, int grid, cudaStream_t s);
 cudaError_t prog_scan(const uint32_t *size16, uint32_t *off16, uint64_t n, void *tmp, size_t *tmp_bytes,
                       cudaStream_t s);
-cudaError_t prog_write(const P2Args &a, const uint32_t *order, const uint32_t *off16, uint4 *prog, int grid,
-                       cudaStream_t s);
-cudaError_t sweep(const S2Args &a, int mode, int grid, cudaStream_t s);
 cudaError_t prog_max(const uint32_t *size16, uint32_t *out, uint64_t n, void *tmp, size_t *tmp_bytes, cudaStream_t s);
-size_t sweep_smem(uint32_t maxrec);
 cudaError_t scalars(int N, int full_lists, double Lam, int mode, int c, uint32_t active, int ncta,
                     const double *partial, double *blk, cudaStream_t s, int transposed = 0,
                     double *blk_out = nullptr);   // blk_out: write the updated block there instead of in place

@@ -2056,15 +2056,21 @@ size_t loop_smem(int nW, uint32_t maxblk16) {
 // staged program capacity (records per tile block): as large as fits, at most the largest
 // block (measured: staging every program beats more resident CTAs per SM); the device-resident
 // solve needs loop_smem - sweep_smem more shared memory
+// shared memory one CTA may use: the whole SM (less 4 KB) at one CTA per SM, an equal share
+// of the 228 KB array (less the 1 KB per-CTA reservation and the static shared memory) at more
+static size_t smem_budget(int nW, bool dev_loop) {
+    const int cps = dev_loop ? 1 : ctas_per_sm(nW);
+    return cps == 1 ? 224u * 1024u - 2048u : (size_t)(228u * 1024u) / cps - 4096u;
+}
 uint32_t choose_cap(int nW, uint32_t maxblk16, bool dev_loop) {
-    const size_t budget = 224u * 1024u - 2048u;
+    const size_t budget = smem_budget(nW, dev_loop);
     const size_t fixed = dev_loop ? loop_smem(nW, 0) : sweep_smem(nW, 0);
     if (fixed >= budget) return 0;
     const size_t cap = (budget - fixed) / (2 * 16);
     return (uint32_t)std::min<size_t>(cap, maxblk16);
 }
 bool fits_smem(int nW, uint32_t maxblk16, bool dev_loop) {
-    return (dev_loop ? loop_smem(nW, maxblk16) : sweep_smem(nW, maxblk16)) <= 224u * 1024u;
+    return (dev_loop ? loop_smem(nW, maxblk16) : sweep_smem(nW, maxblk16)) <= smem_budget(nW, dev_loop) + 2048u;
 }
 
 cudaError_t prog_count(const P3Args &a, const uint32_t *order, uint32_t *size16, int *err, int grid, cudaStream_t s) {
@@ -2084,7 +2090,7 @@ static cudaError_t launch(const S3Args &a, int grid, cudaStream_t s) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
     // leave the rest of the unified L1/shared array to L1
-    const int carve = (int)std::min<size_t>(100, (sm + 2048) * 100 / (228 * 1024) + 1);
+    const int carve = (int)std::min<size_t>(100, (sm + 2048) * ctas_per_sm(a.nW) * 100 / (228 * 1024) + 1);
     e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
     if (e != cudaSuccess) return e;
     kern<<<grid, 32 << a.nW, sm, s>>>(a);

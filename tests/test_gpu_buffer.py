@@ -102,7 +102,7 @@ def test_buffer_cfg3_against_fixture(hq, C):
 
 @pytest.mark.parametrize("N", [3, 5, 8])
 def test_buffer_small_paths(hq, N):
-    """The two-pass path (N < 8) and the warp-tiled path (N = 8) take the same waiting room."""
+    """The two-pass path (N <= 8) takes the same waiting room as the tiled path."""
     inst = hqinst.generate(N, 6, seed=N, rho=0.8)
     for C in (2, U):
         g = gpu_solve_buffer(hq, inst, C)

@@ -126,6 +126,37 @@ def test_cfg3_whole_vector(hq):
         whole_vector(g, o, inst)
 
 
+def gpu_solve_env(hq, inst, env):
+    """gpu_solve with development switches set in the environment (read at hq_create)."""
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        return gpu_solve(hq, inst)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k)
+            else:
+                os.environ[k] = v
+
+
+@pytest.mark.parametrize("order", [
+    {"HQ_ORDER": "group", "HQ_GROUP_BITS": "3"},                          # cfg4/cfg5 default path
+    {"HQ_ORDER": "group", "HQ_GROUP_BITS": "4", "HQ_PFH": "0", "HQ_PFO": "0"},
+    {"HQ_ORDER": "chunk", "HQ_CHUNK_BITS": "2"},   # 256 chunks >= the 148-CTA grid
+])
+def test_tile_orders_whole_vector(hq, order):
+    """The tile visit orders of N >= 27 (group order: Gray-code groups, round-robin CTAs, L2
+    prefetch of the tile-unit slices; chunked order) at N = 23, where the oracle runs in the
+    session: the order only changes which CTA sums which tile, never a state's arithmetic."""
+    inst = hqinst.config_instance(4, N=23, J=200)
+    g = gpu_solve_env(hq, inst, order)
+    assert g["stats"]["path"] == 3 and g["stats"]["chunk_bits"] >= 0
+    o = oracle.solve(inst, tol=TOL, max_iter=5000)
+    assert o["status"] == 0
+    whole_vector(g, o, inst)
+
+
 @pytest.mark.parametrize("N,cfg,J", [(12, 2, 60), (18, 2, 100), (21, 4, 150)])
 def test_device_loop_matches_host_loop(hq, N, cfg, J):
     """The device-resident solve performs the same half-sweeps as the host-looped one: after a

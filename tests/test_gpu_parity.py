@@ -55,7 +55,9 @@ def test_configs_full_oracle(hq, cfg):
 
 _SMALL = [
     dict(N=6, J=10, clustered=False, L=None),
-    dict(N=9, J=30, clustered=True, L=None),
+    dict(N=8, J=20, clustered=False, L=None),   # largest size of the two-pass path
+    dict(N=8, J=25, clustered=True, L=3),
+    dict(N=9, J=30, clustered=True, L=None),    # smallest size of the tiled path
     dict(N=11, J=40, clustered=False, L=4),
     dict(N=12, J=80, clustered=False, L=None),
     dict(N=13, J=60, clustered=True, L=6),
