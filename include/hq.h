@@ -255,7 +255,9 @@ const char *hq_error_string(hq_handle h);
  *   [17] 1 if the solve ran device-resident (one launch for every half-sweep, check and
  *        residual; [8] and [10] then split [16] by the phases' timestamps), 0 if host-looped,
  *   [18] tile visit order of the CTA-tiled path: -1 popcount order, b >= 0 chunked
- *        order with chunks of 2^b tiles (N >= 27).
+ *        order with chunks of 2^b tiles (N >= 27),
+ *   [19] group progress bound of the group order: a CTA starts a tile of group g only
+ *        when every CTA is done with group g - [19] (0: unbounded).
  */
 #define HQ_STATS_LEN 20
 hq_status hq_stats(hq_handle h, double *out);

@@ -319,6 +319,10 @@ struct hq_problem {
     int pf_h = 0, pf_o = 0;        // path 3: L2 prefetch distance of the tile-unit slices; of omega/kappa
     int in_pol = 0;                // path 3: L2 policy of the q blocks and in-group neighbours (S3Args::pol)
     int pf_min = 0;                // path 3: prefetch only the tile units h >= pf_min
+    // path 3, group order: group progress bound (S3Args::gs_ctr); gs_lag 0 = off
+    int gs_lag = 0;
+    uint32_t gs_ng = 0;
+    unsigned long long *d_gsctr = nullptr, gs_epoch = 0;
     std::vector<uint32_t> chunk_range;   // path 3, chunked order: CTA ranges over the visit order
     uint32_t *d_order = nullptr, *d_off16 = nullptr, *d_size16 = nullptr, *d_range = nullptr;
     uint4 *d_prog = nullptr;
@@ -356,6 +360,9 @@ struct hq_problem {
         d_range = nullptr;
         dfree(d_wtime);
         d_wtime = nullptr;
+        dfree(d_gsctr);
+        d_gsctr = nullptr;
+        gs_epoch = 0;
         dfree(d_off16);
         dfree(d_size16);
         dfree(d_prog);
@@ -918,6 +925,10 @@ static hq_status v3_prepare(hq_problem *h, cudaStream_t s) {
             if (const char *penv = getenv("HQ_HPOL")) h->h_out_pol = atoi(penv);
             h->pf_h = 4;   // measured at cfg5: 4 units ahead -12 % per half-sweep, 6 ahead -9 %
             h->pf_o = 1;
+            h->gs_lag = 0;
+            if (const char *e = getenv("HQ_GLAG")) h->gs_lag = std::max(0, atoi(e));
+            h->gs_ng = (uint32_t)ng;
+            if (h->sgrid > h->nsm) h->gs_lag = 0;   // the bound needs one resident CTA per SM
 
             h->chunk_range.assign(G + 1, 0);
             for (int cta = 0; cta < G; cta++) {
@@ -1036,6 +1047,25 @@ static cudaError_t tiled_sweep(hq_problem *h, const S2Args &sa, int mode, cudaSt
     a.in_pol = h->in_pol;
     a.pf_min = h->pf_min;
     a.pf_o = h->pf_o;
+    if (h->gs_lag > 0 && h->chunked && h->gs_ng > 0) {
+        if (!h->d_gsctr) {
+            if (dmalloc((void **)&h->d_gsctr, 8 * (size_t)h->gs_ng) != cudaSuccess ||
+                cudaMemset(h->d_gsctr, 0, 8 * (size_t)h->gs_ng) != cudaSuccess) {
+                cudaGetLastError();
+                dfree(h->d_gsctr);
+                h->d_gsctr = nullptr;
+                h->gs_lag = 0;   // run without the bound
+            }
+            h->gs_epoch = 0;
+        }
+        if (h->d_gsctr) {
+            a.gs_ctr = h->d_gsctr;
+            a.gs_target = (h->gs_epoch + 1) * (unsigned long long)h->sgrid;
+            a.gs_bits = h->chunk_bits;
+            a.gs_lag = h->gs_lag;
+            a.gs_ng = h->gs_ng;
+        }
+    }
     if (!h->d_wtime && dmalloc((void **)&h->d_wtime, 8 * 4096) == cudaSuccess) cudaMemset(h->d_wtime, 0, 8 * 4096);
     a.wtime = h->d_wtime;
     a.Q = sa.Q;
@@ -1050,7 +1080,12 @@ static cudaError_t tiled_sweep(hq_problem *h, const S2Args &sa, int mode, cudaSt
         a.prev_partial = f->prev_partial;
         a.blk_out = f->blk_out;
     }
-    return hq3_launch::sweep(a, sa.full_lists, mode, h->sgrid, s);
+    const cudaError_t e = hq3_launch::sweep(a, sa.full_lists, mode, h->sgrid, s);
+    if (a.gs_ctr) {
+        if (e == cudaSuccess) h->gs_epoch++;
+        else h->gs_lag = 0;   // a launch that did not run leaves the counters behind: stop using them
+    }
+    return e;
 }
 
 static S2Args base_s2(hq_problem *h) {
@@ -1466,6 +1501,7 @@ static hq_status solve_core(hq_handle h, double tol, int max_iter, double *pi, v
         h->stats[16] = o.kernel_ms >= 0.0 ? o.kernel_ms : 0.0;
         h->stats[17] = o.kernel_ms >= 0.0 ? 1.0 : 0.0;
         h->stats[18] = h->chunked ? h->chunk_bits : -1;
+        h->stats[19] = (h->chunked && h->d_gsctr) ? h->gs_lag : 0;
         if (iters_out) *iters_out = o.sweeps;
         if (residual_out) *residual_out = o.res;
         if (!std::isfinite(o.res)) {

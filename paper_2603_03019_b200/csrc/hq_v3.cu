@@ -487,11 +487,33 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
         if (staged) bulk_g2s(sptr(b + TS), a.prog + o, nrec * 16u, bar);
 #endif
     };
+    // group progress bound (S3Args::gs_ctr): thread 0 only
+    const bool gsy = a.gs_ctr != nullptr;
+    auto grp_of = [&](int k) -> uint32_t {
+        return (uint32_t)(((uint64_t)blockIdx.x + (uint64_t)k * gridDim.x) >> a.gs_bits);
+    };
+    auto gs_done = [&](uint32_t g0, uint32_t g1) {   // this CTA is done with groups [g0, g1)
+        for (uint32_t g = g0; g < g1 && g < a.gs_ng; g++) atomicAdd(a.gs_ctr + g, 1ull);
+    };
+    auto gs_wait = [&](uint32_t g) {   // wait until every CTA is done with group g - gs_lag
+        if (g < (uint32_t)a.gs_lag) return;
+        const unsigned long long *c = a.gs_ctr + (g - (uint32_t)a.gs_lag);
+        while (true) {
+            unsigned long long v;
+            asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(c) : "memory");
+            if (v >= a.gs_target) break;
+            __nanosleep(100);
+        }
+    };
     if (tid == 0) {
         s_done[0] = s_done[1] = 0;
         mbar_init(sptr(&tbar[0]), 1);
         mbar_init(sptr(&tbar[1]), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        if (gsy) {
+            gs_done(0, nt > 0 ? grp_of(0) : a.gs_ng);
+            if (nt > 0) gs_wait(grp_of(0));
+        }
         if (nt > 0) load_tile(0);   // in flight during the prologue
     }
 
@@ -620,9 +642,18 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
         }
 #else
         __syncthreads();   // every warp is done with tile k-1: its buffer may be refilled
-        if (tid == 0 && k + 1 < nt) {
-            fence_proxy_async();
-            load_tile(k + 1);
+        if (tid == 0) {
+            if (gsy && k > 0) {
+                // done with every group before tile k's; then wait until every CTA is done with
+                // group g(k) - lag.  Deadlock-free: each CTA has marked every group below its
+                // pending one, so the CTA with the lowest pending group never waits.
+                if (grp_of(k) != grp_of(k - 1)) gs_done(grp_of(k - 1), grp_of(k));
+                gs_wait(grp_of(k));
+            }
+            if (k + 1 < nt) {
+                fence_proxy_async();
+                load_tile(k + 1);
+            }
         }
 #endif
 #ifdef HQ_WARP_TIMING
@@ -917,6 +948,7 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
 #endif
     }
     flush();
+    if (gsy && tid == 0 && nt > 0) gs_done(grp_of(nt - 1), a.gs_ng);
 #ifdef HQ_WARP_TIMING
     if (MODE == 0 && tid == 0) {   // CTA start / end (globaltimer ns), after the per-warp slots
         unsigned long long t_end;
@@ -2093,6 +2125,11 @@ static cudaError_t launch(const S3Args &a, int grid, cudaStream_t s) {
     const int carve = (int)std::min<size_t>(100, (sm + 2048) * ctas_per_sm(a.nW) * 100 / (228 * 1024) + 1);
     e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
     if (e != cudaSuccess) return e;
+    if (a.gs_ctr) {   // group progress bound: the CTAs wait on each other, all must be resident
+        S3Args ac = a;
+        void *args[] = {(void *)&ac};
+        return cudaLaunchCooperativeKernel((const void *)kern, dim3(grid), dim3(32 << a.nW), args, sm, s);
+    }
     kern<<<grid, 32 << a.nW, sm, s>>>(a);
     return cudaGetLastError();
 }

@@ -85,6 +85,17 @@ struct S3Args {
     int pf_h;                // > 0: L2 prefetch of the tile-unit neighbour slices pf_h units ahead
     int pf_o;                // 1: L2 prefetch of the tile's scatter weights before the tile units
     int pf_min;              // prefetch only the tile units h >= pf_min
+    // group progress bound (group order): CTA b's k-th tile is the
+    // (b + k G)-th of the group-major sequence, group (b + k G) >> gs_bits.  A CTA adds 1 to
+    // gs_ctr[g] once it is done with its tiles of group g (at once for groups it has no tile
+    // in), and its thread 0 goes on with a tile of group g only when every CTA is done with
+    // group g - gs_lag (gs_ctr[g - gs_lag] >= gs_target = launches x G: the counters are never
+    // reset).  Only the visit timing changes, never a CTA's tiles or its summation order.
+    // Needs every CTA resident (cooperative launch).
+    unsigned long long *gs_ctr;   // [gs_ng] or nullptr (off)
+    unsigned long long gs_target;
+    int gs_bits, gs_lag;
+    uint32_t gs_ng;
     // folded scalar step (MODE 0/1): every CTA first performs the scalar step of the previous
     // half-sweep (class prev_c, layers prev_active) from that launch's transposed partials
     // prev_partial and the block coef; CTA 0 stores the updated block in blk_out

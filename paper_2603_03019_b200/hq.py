@@ -321,7 +321,8 @@ class Solver:
         s = hq_stats(self.h)
         keys = ["sweeps", "halfsweeps", "state_updates", "launches", "residual_evals", "trie_nodes", "sum_pi_minus_1",
                 "solve_ms", "sweep_ms", "sweep_launches", "residual_ms", "precompute_ms", "program_bytes", "path",
-                "max_program_block", "program_nwv", "solve_kernel_ms", "device_loop", "chunk_bits"]
+                "max_program_block", "program_nwv", "solve_kernel_ms", "device_loop", "chunk_bits",
+                "group_lag"]
         return {k: float(s[i]) for i, k in enumerate(keys)}
 
     def close(self):

@@ -59,8 +59,22 @@ def main(which):
         nrand = 20000
     else:
         raise SystemExit("unknown fixture " + which)
+    # the oracle's Algorithm-3 rate table (2^N N doubles, same arithmetic as its list scans)
+    # when the host has the memory for it: cfg4 needs 60 GB + ~20 GB of other arrays
+    need = (1 << inst.N) * inst.N * 8 + (1 << inst.N) * 8 * 10
+    use_table = None
+    try:
+        with open("/proc/meminfo") as fh:
+            avail = [int(x.split()[1]) * 1024 for x in fh if x.startswith("MemAvailable")][0]
+        use_table = avail > 1.2 * need
+    except (OSError, IndexError):
+        pass
+    if inst.N >= 27 and not use_table:
+        raise SystemExit(f"{which}: the list-scan oracle at N = {inst.N} takes days; needs "
+                         f"{1.2 * need / 2**30:.0f} GB of host memory for the rate table")
+    print(f"{which}: N={inst.N} J={inst.J} use_table={use_table} threads={oracle.num_threads()}", flush=True)
     t = time.time()
-    r = oracle.solve(inst, tol=1e-13, max_iter=3000)
+    r = oracle.solve(inst, tol=1e-13, max_iter=3000, use_table=use_table)
     dt = time.time() - t
     pi = r["pi"]
     N = inst.N
@@ -77,7 +91,8 @@ def main(which):
     out = os.path.join(HERE, f"oracle_{which}.npz")
     np.savez_compressed(out, sha256=inst.sha256(), iters=r["iters"], residual=r["residual"], status=r["status"],
                         masses=masses, workload=w, dispatch=d, loss=loss, states=st, pi_states=pi[st],
-                        oracle_seconds=dt, oracle_threads=oracle.num_threads(), tol=1e-13, **extra)
+                        oracle_seconds=dt, oracle_threads=oracle.num_threads(), tol=1e-13,
+                        oracle_table=bool(use_table), **extra)
     print(f"wrote {out}: iters={r['iters']} residual={r['residual']:.3e} time={dt:.1f}s threads={oracle.num_threads()}")
 
 

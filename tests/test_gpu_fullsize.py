@@ -144,6 +144,7 @@ def gpu_solve_env(hq, inst, env):
     {"HQ_ORDER": "group", "HQ_GROUP_BITS": "3"},                          # cfg4/cfg5 default path
     {"HQ_ORDER": "group", "HQ_GROUP_BITS": "4", "HQ_PFH": "0", "HQ_PFO": "0"},
     {"HQ_ORDER": "chunk", "HQ_CHUNK_BITS": "2"},   # 256 chunks >= the 148-CTA grid
+    {"HQ_ORDER": "group", "HQ_GROUP_BITS": "3", "HQ_GLAG": "1"},          # group progress bound
 ])
 def test_tile_orders_whole_vector(hq, order):
     """The tile visit orders of N >= 27 (group order: Gray-code groups, round-robin CTAs, L2
@@ -237,3 +238,18 @@ def test_cfg5_homogeneous_erlang(hq):
     N = inst.N
     w = np.array([math.exp(n * math.log(a) - math.lgamma(n + 1)) for n in range(N + 1)])
     np.testing.assert_allclose(layer_masses_np(g["pi"], N), w / w.sum(), rtol=0, atol=PI_MAX)
+
+
+@pytest.mark.parametrize("gb,lag", [(3, 1), (3, 2), (6, 1)])
+def test_group_lag_bitwise(hq, gb, lag):
+    """The group progress bound (HQ_GLAG: a CTA starts a tile of group g only when every CTA
+    is done with group g - lag) changes when a CTA visits its tiles, never which tiles or in
+    which order it sums them: pi and the measures are bitwise those of the unbounded run."""
+    inst = hqinst.config_instance(4, N=23, J=200)
+    base = {"HQ_ORDER": "group", "HQ_GROUP_BITS": str(gb)}
+    g0 = gpu_solve_env(hq, inst, base)
+    g1 = gpu_solve_env(hq, inst, dict(base, HQ_GLAG=str(lag)))
+    assert g0["stats"]["group_lag"] == 0 and g1["stats"]["group_lag"] == lag
+    assert g0["iters"] == g1["iters"] and g0["residual"] == g1["residual"]
+    assert np.array_equal(g0["pi"], g1["pi"])
+    assert np.array_equal(g0["workload"], g1["workload"]) and g0["loss"] == g1["loss"]
