@@ -1047,6 +1047,9 @@ static cudaError_t tiled_sweep(hq_problem *h, const S2Args &sa, int mode, cudaSt
     a.in_pol = h->in_pol;
     a.pf_min = h->pf_min;
     a.pf_o = h->pf_o;
+    a.pol_q = a.pol[a.in_pol & 3];
+    a.pol_hout = a.pol[a.h_out_pol & 3];
+    a.pol_ef = a.pol[2];
     if (h->gs_lag > 0 && h->chunked && h->gs_ng > 0) {
         if (!h->d_gsctr) {
             if (dmalloc((void **)&h->d_gsctr, 8 * (size_t)h->gs_ng) != cudaSuccess ||

@@ -228,6 +228,9 @@ __device__ __forceinline__ double unit_rates(const Prog<WP> &P, const uint4 &h, 
         d += 8;
     }
     const int ng = (int)(inf & 0xffu);
+#ifdef HQ_COMPACT
+#pragma unroll 1
+#endif
     for (int g = 0; g < ng; g++) {
         const uint32_t hd = d->x;
         const uint32_t M = (hd >> 16) & 0x1ffu;
@@ -435,7 +438,9 @@ __device__ __forceinline__ void flush_fast3(const uint64_t *tab, int p0, int L0,
 
 // ST: every program block is staged (host-checked S3Args::all_staged): program reads are
 // plain shared-memory loads with 32-bit addressing
-template <int MODE, bool FULL, bool WP, bool ST>
+// NWC: log2(warps per CTA) as a compile-time constant (4: the N >= 21 geometry -- the warp-unit
+// loop unrolls and every tile shift is an immediate), 0: taken from S3Args::nW
+template <int MODE, bool FULL, bool WP, bool ST, int NWC = 0>
 __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
     using SL = Slots<MODE, FULL>;
     constexpr int NB = SL::NB;
@@ -447,7 +452,7 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
     __shared__ uint8_t s_pextw[16 * 16];  // [M4][warp] = pext(warp, M4)
     __shared__ uint64_t s_fl[64];         // flush entry lists (flush_table3)
 
-    const int nW = a.nW, T = 8 + nW, NVU = 9 + nW, nH = a.N - NVU;
+    const int nW = NWC ? NWC : a.nW, T = 8 + nW, NVU = 9 + nW, nH = a.N - NVU;
     const int tid = threadIdx.x, lane = tid & 31, warp = wuni(tid >> 5);
     const unsigned nwarps = 1u << nW;
     const uint32_t TS = 1u << T;
@@ -477,7 +482,7 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
         double *b = tileq + (size_t)buf * BUFD;
         mbar_expect(bar, TS * 8u + (staged ? nrec * 16u : 0u));
 #ifndef HQ_NO_L2POL
-        bulk_g2s_pol(sptr(b), a.Q + ((size_t)t << T), TS * 8u, bar, a.pol[a.in_pol]);
+        bulk_g2s_pol(sptr(b), a.Q + ((size_t)t << T), TS * 8u, bar, a.pol_q);
 #else
         bulk_g2s(sptr(b), a.Q + ((size_t)t << T), TS * 8u, bar);
 #endif
@@ -578,10 +583,26 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
     const double nu0 = a.nu[0];
     // L2 policies: kernel parameters (uniform registers; hq3_launch::policies), so that the
     // cache-hinted loads need no per-load register-to-uniform moves
-    const uint64_t pol_ef = a.pol[2], pol_el = a.pol[a.in_pol];
-    const uint64_t pol_out = a.pol[a.h_out_pol];
-    auto hpol = [&](int h) -> uint64_t { return h < a.h_in ? pol_el : pol_out; };
+    const uint64_t pol_ef = a.pol_ef, pol_el = a.pol_q, pol_out = a.pol_hout;
+    // tile-unit neighbour slice of unit h into hb: the policy is chosen by a uniform branch
+    // (two load groups with a fixed uniform policy operand each, no per-load select)
+    auto hload = [&](const double *src, int h, double2 (&hb)[4]) {
+        if (h < a.h_in) {
+#pragma unroll
+            for (int kk = 0; kk < 4; kk++) hb[kk] = ldg2(src + (kk << 6), pol_el);
+        } else {
+#pragma unroll
+            for (int kk = 0; kk < 4; kk++) hb[kk] = ldg2(src + (kk << 6), pol_out);
+        }
+    };
+    // L2 prefetch of the tile-unit slices: lanes 0..15 cover unit h + pf_h, lanes 16..31 unit
+    // h + pf_h + 1 (one 128-byte line each = the warp's 2 KB slice), once per pair of units
+    const int pf_hh = a.pf_h + (lane >> 4);
+    const uint32_t pf_lo = ((uint32_t)warp << 8) | ((uint32_t)(lane & 15) << 4);
 
+    // every layer 1..N-1 of the updated class is active (steady state of the schedule)
+    const uint32_t class_layers = (a.c ? 0xaaaaaaaau : 0x55555555u) & (((1u << a.N) - 1u) & ~1u);   // N <= 31
+    const bool all_active = (a.active & class_layers) == class_layers;
     double acc[NB];   // lane L: layer L
 #pragma unroll
     for (int v = 0; v < NB; v++) acc[v] = 0.0;
@@ -600,9 +621,20 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
         flush_fast3<NB>(s_fl, p0, L0, lane, tid, nthr, sb, fscr, acc);
     };
 
+    // tile index and program offsets of the next tile, loaded one tile ahead (their L2
+    // latency is off the tile's critical path): t, block start, this warp's program, block end
+    uint32_t t_nx = 0, o0_nx = 0, ow_nx = 0, oe_nx = 0;
+    auto tile_meta = [&](uint32_t tidx) {
+        const uint64_t widx = (uint64_t)tidx << nW;
+        t_nx = __ldg(a.order + tidx);
+        o0_nx = __ldg(a.off16 + widx);
+        ow_nx = __ldg(a.off16 + widx + warp);
+        if (!ST) oe_nx = widx + nwarps < nwt ? __ldg(a.off16 + widx + nwarps) : a.total16;
+    };
+    if (nt > 0) tile_meta(i0);
     for (int k = 0; k < nt; k++) {
         const uint32_t tidx = i0 + k;
-        const uint32_t t = __ldg(a.order + tidx);
+        const uint32_t t = t_nx;
         const uint32_t jt = t << T;
         const int buf = k & 1;
         // tile-unit neighbour slices: three rotating buffers, each consumed in place and then
@@ -613,14 +645,10 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
 #ifdef HQ_HBUF3
         double2 hb2[4];
 #endif
-        if (nH > 0) {
-#pragma unroll
-            for (int kk = 0; kk < 4; kk++) hb0[kk] = ldg2(hsrc(0) + (kk << 6), hpol(0));
-        }
-        if (nH > 1) {
-#pragma unroll
-            for (int kk = 0; kk < 4; kk++) hb1[kk] = ldg2(hsrc(1) + (kk << 6), hpol(1));
-        }
+        if (nH > 0) hload(hsrc(0), 0, hb0);
+#ifndef HQ_H1
+        if (nH > 1) hload(hsrc(1), 1, hb1);
+#endif
         mbar_wait(sptr(&tbar[buf]), (unsigned)((k >> 1) & 1));
 #ifdef HQ_LASTWARP
         // no CTA barrier: each warp reports that it is done with tile k-1 (buffer buf ^ 1);
@@ -660,15 +688,9 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
         const long long tw0 = clock64();
 #endif
         const double *tq = tileq + (size_t)buf * BUFD;
-        uint32_t o0, ow;
-        bool staged;
-        {
-            const uint64_t widx = (uint64_t)tidx << nW;
-            o0 = __ldg(a.off16 + widx);
-            ow = __ldg(a.off16 + widx + warp);
-            const uint32_t nrec = (widx + nwarps < nwt ? __ldg(a.off16 + widx + nwarps) : a.total16) - o0;
-            staged = ST || nrec <= a.maxblk16;
-        }
+        const uint32_t o0 = o0_nx, ow = ow_nx;
+        const bool staged = ST || oe_nx - o0 <= a.maxblk16;
+        if (k + 1 < nt) tile_meta(tidx + 1);
         const int K = __popc(t);
         if (K != curK) {
             flush();
@@ -730,7 +752,11 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
             }
         }
         // ---- lane units 2..6 (lane bits 0..4): busy per lane
+#ifdef HQ_COMPACT   // one copy of the unit body (code size: the tile loop exceeds the instruction caches)
+#pragma unroll 1
+#else
 #pragma unroll
+#endif
         for (int b = 0; b < 5; b++) {
             const int u = 2 + b;
             const bool busy = (lane >> b) & 1;
@@ -775,19 +801,10 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
         // ---- tile units (H): two buffers, copied out before the refill two units ahead
         auto unit_H = [&](int h, double2 (&hb)[4]) {
             const int u = NVU + h;
-            // L2 prefetch of this warp's 2 KB slice of the neighbour block pf_h units ahead
-            // (16 lanes, one 128-byte line each)
-            if (a.pf_h && h + a.pf_h < nH && h + a.pf_h >= a.pf_min && lane < 16)
-                prefetch_l2line(a.Q + ((jt ^ (1u << (T + h + a.pf_h))) | ((uint32_t)warp << 8)) + lane * 16);
             double2 qq[4];
 #pragma unroll
             for (int kk = 0; kk < 4; kk++) qq[kk] = hb[kk];
-            if (h + 2 < nH) {
-                const double *src = hsrc(h + 2);
-                const uint64_t pl2 = hpol(h + 2);
-#pragma unroll
-                for (int kk = 0; kk < 4; kk++) hb[kk] = ldg2(src + (kk << 6), pl2);
-            }
+            if (h + 2 < nH) hload(hsrc(h + 2), h + 2, hb);
             if ((t >> h) & 1u) {
                 const uint4 hu = P.hdr(u);
                 const double Wt = unit_rates(P, hu, sh, hdr_w0(hu), qq, A);
@@ -801,10 +818,39 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
         };
         if (MODE < 2 && a.pf_o)   // this warp's 4 KB of scatter weights, needed in the epilogue
             prefetch_l2line(a.omkap + (jt | ((uint32_t)warp << 8)) + lane * 8);
+#ifdef HQ_H1   // one buffer, refilled one unit ahead: one copy of the unit body, 16 fewer registers
+#pragma unroll 1
+        for (int h = 0; h < nH; h++) {
+            if (a.pf_h && !(h & 1)) {
+                const int hh = h + pf_hh;
+                if (hh < nH && hh >= a.pf_min) prefetch_l2line(a.Q + ((jt ^ (1u << (T + hh))) | pf_lo));
+            }
+            const int u = NVU + h;
+            double2 qq[4];
+#pragma unroll
+            for (int kk = 0; kk < 4; kk++) qq[kk] = hb0[kk];
+            if (h + 1 < nH) hload(hsrc(h + 1), h + 1, hb0);
+            if ((t >> h) & 1u) {
+                const uint4 hu = P.hdr(u);
+                const double Wt = unit_rates(P, hu, sh, hdr_w0(hu), qq, A);
+#pragma unroll
+                for (int r = 0; r < R; r++) A[r] = fma(Wt, qv(qq, r), A[r]);
+            } else {
+                const double nuu = a.nu[u];
+#pragma unroll
+                for (int r = 0; r < R; r++) D[r] = fma(nuu, qv(qq, r), D[r]);
+            }
+        }
+#else
         for (int h = 0; h < nH; h += 2) {
+            if (a.pf_h) {   // L2 prefetch of the slices of units h + pf_h, h + pf_h + 1
+                const int hh = h + pf_hh;
+                if (hh < nH && hh >= a.pf_min) prefetch_l2line(a.Q + ((jt ^ (1u << (T + hh))) | pf_lo));
+            }
             unit_H(h, hb0);
             if (h + 1 < nH) unit_H(h + 1, hb1);
         }
+#endif
 #else
         // ---- tile units (H): neighbour tile slices straight from global memory (L2)
         auto unit_H = [&](int h, double2 (&hb)[4]) {
@@ -823,21 +869,11 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
 #pragma unroll
                 for (int r = 0; r < R; r++) D[r] = fma(nuu, qv(hb, r), D[r]);
             }
-            if (h + 3 < nH) {
-                const double *src = hsrc(h + 3);
-                const uint64_t pl3 = hpol(h + 3);
-#pragma unroll
-                for (int kk = 0; kk < 4; kk++) hb[kk] = ldg2(src + (kk << 6), pl3);
-            }
+            if (h + 3 < nH) hload(hsrc(h + 3), h + 3, hb);
         };
         if (MODE < 2 && a.pf_o)   // this warp's 4 KB of scatter weights, needed in the epilogue
             prefetch_l2line(a.omkap + (jt | ((uint32_t)warp << 8)) + lane * 8);
-        if (nH > 2) {
-            const double *src = hsrc(2);
-            const uint64_t pl2 = hpol(2);
-#pragma unroll
-            for (int kk = 0; kk < 4; kk++) hb2[kk] = ldg2(src + (kk << 6), pl2);
-        }
+        if (nH > 2) hload(hsrc(2), 2, hb2);
         for (int h = 0; h < nH; h += 3) {
             unit_H(h, hb0);
             if (h + 1 < nH) unit_H(h + 1, hb1);
@@ -861,16 +897,19 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
 #pragma unroll
             for (int r = 0; r < R; r++) lam[r] = a.Lam - (lam[r] + Bt);
         }
-        // ---- epilogue
+        // ---- epilogue (AA: every state of the tile is updated -- all layers of the class active
+        // and no single-state layer 0 / N in the tile: no per-state selects, unconditional stores)
+        auto epilogue = [&](auto aa) {
+        constexpr bool AA = decltype(aa)::value;
         const int base = K + popc_t;
         const double mu_base = mu_F + mu_t;
+        // this thread's slot in the updated class and its scatter weights: one 64-bit base each,
+        // the 8 states at immediate offsets
+        double *const Pb = a.P + (size_t)(jt | jw);
+        const double2 *const okb = a.omkap + (size_t)(jt | jw);
         double pnew[R];
         bool act[R];
-        double bins[3][NB];
-#pragma unroll
-        for (int h = 0; h < 3; h++)
-#pragma unroll
-            for (int v = 0; v < NB; v++) bins[h][v] = 0.0;
+        double bins[3][NB], spc[4][NB];
 #pragma unroll
         for (int r = 0; r < R; r++) {
             const int pc = __popc(r);
@@ -880,8 +919,8 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
             double lm = lam[r];
             if (FULL && n == a.N) lm = 0.0;
             const double den = lm + mu;
-            const uint32_t j = jt + (jw | ((r >> 1) << 6) | (r & 1));
-            const double pold = MODE >= 1 ? __ldg(a.P + j) : 0.0;
+            const int jr = ((r >> 1) << 6) | (r & 1);
+            const double pold = MODE >= 1 ? __ldg(Pb + jr) : 0.0;
             double val[NB];
             act[r] = true;
             if (MODE == 2) {
@@ -890,9 +929,9 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
                 val[0] = fabs(out - in);
                 val[1] = out;
             } else {
-                act[r] = (a.active >> n) & 1u;
+                act[r] = AA ? true : (((a.active >> n) & 1u) != 0);
                 const double p = (s_x[n] * A[r] + s_y[n] * D[r]) * rcp_nr(den);
-                const double2 ok = ldg2p(a.omkap + j, pol_ef);
+                const double2 ok = ldg2p(okb + jr, pol_ef);
                 pnew[r] = p;
                 val[0] = act[r] ? p : 0.0;
                 val[1] = act[r] ? p * ok.x : 0.0;
@@ -901,19 +940,18 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
                 if (!FULL) val[v++] = act[r] ? p * lm : 0.0;
                 if (MODE == 1) val[v++] = act[r] ? fabs(p - pold) : 0.0;
             }
-            // bin h(r) = (pc + 1 - beta) >> 1
+            // bin h(r) = (pc + 1 - beta) >> 1: summed per popcount of r here, assigned below
 #pragma unroll
             for (int v = 0; v < NB; v++) {
-                if (pc == 0) bins[0][v] += val[v];
-                else if (pc == 2) bins[1][v] += val[v];
-                else if (pc == 1) {
-                    if (beta) bins[0][v] += val[v];
-                    else bins[1][v] += val[v];
-                } else {
-                    if (beta) bins[1][v] += val[v];
-                    else bins[2][v] += val[v];
-                }
+                if (r == 0 || r == 1 || r == 3 || r == 7) spc[pc][v] = val[v];   // first state of its popcount
+                else spc[pc][v] += val[v];
             }
+        }
+#pragma unroll
+        for (int v = 0; v < NB; v++) {   // pc 0 -> bin 0, pc 2 -> bin 1, pc 1 -> bin 1 - beta, pc 3 -> bin 2 - beta
+            bins[0][v] = spc[0][v] + (beta ? spc[1][v] : 0.0);
+            bins[1][v] = spc[2][v] + (beta ? spc[3][v] : spc[1][v]);
+            bins[2][v] = beta ? 0.0 : spc[3][v];
         }
 #pragma unroll
         for (int h = 0; h < 3; h++)
@@ -926,7 +964,7 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
         if (MODE < 2) {
 #pragma unroll
             for (int kk = 0; kk < 4; kk++) {
-                double *dst = a.P + (jt + (jw | (kk << 6)));
+                double *dst = Pb + (kk << 6);
                 if (act[2 * kk] && act[2 * kk + 1]) {
 #ifndef HQ_NO_L2POL
                     stg2_pol(dst, pnew[2 * kk], pnew[2 * kk + 1], pol_ef);
@@ -939,6 +977,12 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
                 }
             }
         }
+        };
+#ifndef HQ_NO_AA
+        if (MODE < 2 && all_active && t != 0 && t != (uint32_t)a.ntiles - 1) epilogue(std::true_type{});
+        else
+#endif
+            epilogue(std::false_type{});
         };
 #ifdef HQ_NO_SPLIT
         body(std::integral_constant<int, 2>{});
@@ -2115,10 +2159,10 @@ cudaError_t prog_write(const P3Args &a, const uint32_t *order, const uint32_t *o
     return cudaGetLastError();
 }
 
-template <int MODE, bool FULL, bool WP, bool ST>
+template <int MODE, bool FULL, bool WP, bool ST, int NWC = 0>
 static cudaError_t launch(const S3Args &a, int grid, cudaStream_t s) {
     const size_t sm = sweep_smem(a.nW, a.maxblk16);
-    auto kern = hq3::k_sweep3<MODE, FULL, WP, ST>;
+    auto kern = hq3::k_sweep3<MODE, FULL, WP, ST, NWC>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
     // leave the rest of the unified L1/shared array to L1
@@ -2136,6 +2180,12 @@ static cudaError_t launch(const S3Args &a, int grid, cudaStream_t s) {
 
 template <bool WP, bool ST>
 static cudaError_t sweep_st(const S3Args &a, int full, int mode, int grid, cudaStream_t s) {
+#ifndef HQ_NO_NWC
+    if (WP && a.nW == 4 && mode < 2) {   // the N >= 21 geometry with warp programs: nW a compile-time constant
+        if (full) return mode == 0 ? launch<0, true, WP, ST, WP ? 4 : 0>(a, grid, s) : launch<1, true, WP, ST, WP ? 4 : 0>(a, grid, s);
+        return mode == 0 ? launch<0, false, WP, ST, WP ? 4 : 0>(a, grid, s) : launch<1, false, WP, ST, WP ? 4 : 0>(a, grid, s);
+    }
+#endif
     if (full) {
         if (mode == 0) return launch<0, true, WP, ST>(a, grid, s);
         if (mode == 1) return launch<1, true, WP, ST>(a, grid, s);

@@ -82,6 +82,11 @@ struct S3Args {
     int h_out_pol;
     uint64_t pol[4];         // L2 policy encodings: evict-last, evict-normal, evict-first, half evict-last
     int in_pol;              // policy (index into pol) of the q blocks and the neighbours h < h_in
+    // the three policies the sweep kernel uses, resolved by the host (plain parameters: the
+    // cache-hinted loads take them from uniform registers without a per-load select)
+    uint64_t pol_q;          // = pol[in_pol]: q blocks, tile-unit neighbours h < h_in
+    uint64_t pol_hout;       // = pol[h_out_pol]: tile-unit neighbours h >= h_in
+    uint64_t pol_ef;         // = pol[2]: streamed operands (programs, omega/kappa, stores)
     int pf_h;                // > 0: L2 prefetch of the tile-unit neighbour slices pf_h units ahead
     int pf_o;                // 1: L2 prefetch of the tile's scatter weights before the tile units
     int pf_min;              // prefetch only the tile units h >= pf_min
