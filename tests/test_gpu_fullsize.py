@@ -186,6 +186,37 @@ def test_device_loop_matches_host_loop(hq, N, cfg, J):
         whole_vector(gpu_solve_loop(hq, inst, loop), o, inst)
 
 
+def _mem_available():
+    try:
+        with open("/proc/meminfo") as fh:
+            return [int(x.split()[1]) * 1024 for x in fh if x.startswith("MemAvailable")][0]
+    except (OSError, IndexError):
+        return 0
+
+
+def test_n28_iterates_whole_vector(hq):
+    """The N >= 27 launch configuration (group tile order, L2 prefetch, 2^28 states: cfg4's
+    generator with full lists) element by element: after exactly K sweeps the GPU iterate
+    equals the oracle's K-th Algorithm-1 iterate over the WHOLE vector.
+    The oracle needs its rate table here (60 GB + ~20 GB of arrays; list scans take hours)."""
+    inst = hqinst.generate(28, 500, seed=4, rho=0.8, name="cfg4-full-lists")
+    need = (1 << inst.N) * inst.N * 8 + (1 << inst.N) * 8 * 10
+    if _mem_available() < 1.2 * need:
+        pytest.skip("host memory below %.0f GB" % (1.2 * need / 2**30))
+    K = 3
+    o = oracle.solve(inst, tol=0.0, max_iter=K, use_table=True)
+    s = hq.Solver.from_instance(inst)
+    r = s.solve(tol=0.0, max_iter=K)
+    assert r["iters"] == K
+    pi = r["pi"].cpu().numpy()
+    s.close()
+    d = np.abs(pi - o["pi"])
+    assert d.max() <= 1e-14 and d.sum() <= 1e-12, (d.max(), d.sum())
+    # entries are ~4e-9 at this size: also element by element in relative terms
+    rel = float((d / o["pi"]).max())
+    assert o["pi"].min() > 0 and rel <= 1e-9, rel
+
+
 def test_cfg4_against_oracle_fixture(hq):
     if not os.path.exists(GOLD4):
         pytest.skip("tests/golden/oracle_cfg4.npz not generated")

@@ -7,7 +7,7 @@ tail -4 gpurun_out/u2_pytest.log
 timeout 900 python tools/ab.py run 3 3 main m3 m2 m1 base hbuf3 compact h1 hbuf3c > gpurun_out/u2_ab_cfg3.log 2>&1; echo ab3=$?
 cat gpurun_out/u2_ab_cfg3.log
 V=/root/repo/variants
-ROUNDS=2 REPS=2 timeout 1500 python tools/env_ab.py 5 20 main: m3:HQ_LIB=$V/libhq_m3.so m2:HQ_LIB=$V/libhq_m2.so m1:HQ_LIB=$V/libhq_m1.so base:HQ_LIB=$V/libhq_base.so hbuf3:HQ_LIB=$V/libhq_hbuf3.so compact:HQ_LIB=$V/libhq_compact.so h1:HQ_LIB=$V/libhq_h1.so hbuf3c:HQ_LIB=$V/libhq_hbuf3c.so > gpurun_out/u2_ab_cfg5.jsonl 2>&1; echo ab5=$?
+ROUNDS=2 REPS=2 timeout 1700 python tools/env_ab.py 5 20 main: m3:HQ_LIB=$V/libhq_m3.so m2:HQ_LIB=$V/libhq_m2.so m1:HQ_LIB=$V/libhq_m1.so base:HQ_LIB=$V/libhq_base.so hbuf3:HQ_LIB=$V/libhq_hbuf3.so compact:HQ_LIB=$V/libhq_compact.so h1:HQ_LIB=$V/libhq_h1.so hbuf3c:HQ_LIB=$V/libhq_hbuf3c.so pf2:HQ_PFH=2 pf3:HQ_PFH=3 pf6:HQ_PFH=6 pf0:HQ_PFH=0 lag2:HQ_GLAG=2 > gpurun_out/u2_ab_cfg5.jsonl 2>&1; echo ab5=$?
 cat gpurun_out/u2_ab_cfg5.jsonl
 ROUNDS=2 REPS=2 timeout 600 python tools/env_ab.py 4 40 main: m3:HQ_LIB=$V/libhq_m3.so m2:HQ_LIB=$V/libhq_m2.so m1:HQ_LIB=$V/libhq_m1.so base:HQ_LIB=$V/libhq_base.so hbuf3:HQ_LIB=$V/libhq_hbuf3.so compact:HQ_LIB=$V/libhq_compact.so h1:HQ_LIB=$V/libhq_h1.so hbuf3c:HQ_LIB=$V/libhq_hbuf3c.so > gpurun_out/u2_ab_cfg4.jsonl 2>&1; echo ab4=$?
 cat gpurun_out/u2_ab_cfg4.jsonl
