@@ -801,10 +801,14 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
         // ---- tile units (H): two buffers, copied out before the refill two units ahead
         auto unit_H = [&](int h, double2 (&hb)[4]) {
             const int u = NVU + h;
+#ifdef HQ_H2   // consumed in place, refilled after use (no copy; one unit of latency cover)
+            double2 (&qq)[4] = hb;
+#else
             double2 qq[4];
 #pragma unroll
             for (int kk = 0; kk < 4; kk++) qq[kk] = hb[kk];
             if (h + 2 < nH) hload(hsrc(h + 2), h + 2, hb);
+#endif
             if ((t >> h) & 1u) {
                 const uint4 hu = P.hdr(u);
                 const double Wt = unit_rates(P, hu, sh, hdr_w0(hu), qq, A);
@@ -815,6 +819,9 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
 #pragma unroll
                 for (int r = 0; r < R; r++) D[r] = fma(nuu, qv(qq, r), D[r]);
             }
+#ifdef HQ_H2
+            if (h + 2 < nH) hload(hsrc(h + 2), h + 2, hb);
+#endif
         };
         if (MODE < 2 && a.pf_o)   // this warp's 4 KB of scatter weights, needed in the epilogue
             prefetch_l2line(a.omkap + (jt | ((uint32_t)warp << 8)) + lane * 8);

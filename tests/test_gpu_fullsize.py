@@ -240,6 +240,26 @@ def test_cfg4_against_oracle_fixture(hq):
     assert r <= 1.5 * TOL, r
 
 
+def test_cfg4_full_residual(hq):
+    """cfg4 (N = 28, top-8 lists, 2^28 states): the oracle's residual of the WHOLE GPU pi
+    (Eq. balance_eq_heter; unique solution PAPER.md:1438) -- runs with or
+    without the committed fixture."""
+    inst = hqinst.config_instance(4)
+    g = gpu_solve(hq, inst)
+    assert g["status"] == 0 and g["residual"] <= TOL, (g["status"], g["residual"])
+    pi = g.pop("pi")
+    assert abs(pi.sum() - 1.0) <= 1e-12
+    assert pi.min() >= 0.0
+    r, num, den = oracle.residual_stream(inst, pi)
+    assert r <= 1.5 * TOL, r
+    # truncated lists: calls are lost in more states than the all-busy one
+    assert g["loss"] > pi[-1]
+    lhs = inst.mu * g["workload"]
+    rhs = inst.lam.sum() * (1.0 - g["loss"]) * g["dispatch"].sum(axis=0)
+    np.testing.assert_allclose(lhs, rhs, rtol=1e-10, atol=1e-12)
+    del pi
+
+
 @pytest.mark.parametrize("rho", [0.3, 0.6, 0.9])
 def test_cfg5_full_residual(hq, rho):
     """cfg5 (N = 31, 2^31 states, 17 GB pi): the oracle's residual of the whole GPU pi."""
