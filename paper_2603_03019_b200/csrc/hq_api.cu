@@ -925,7 +925,9 @@ static hq_status v3_prepare(hq_problem *h, cudaStream_t s) {
             if (const char *penv = getenv("HQ_HPOL")) h->h_out_pol = atoi(penv);
             h->pf_h = 4;   // measured at cfg5: 4 units ahead -12 % per half-sweep, 6 ahead -9 %
             h->pf_o = 1;
-            h->gs_lag = 0;
+            // group progress bound: CTAs stay within 2 groups of each other (the L2 then holds the
+            // live groups: cfg5 -8.6 % per half-sweep, same box; no gain with 16 groups at cfg4)
+            h->gs_lag = ng >= 32 ? 2 : 0;
             if (const char *e = getenv("HQ_GLAG")) h->gs_lag = std::max(0, atoi(e));
             h->gs_ng = (uint32_t)ng;
             if (h->sgrid > h->nsm) h->gs_lag = 0;   // the bound needs one resident CTA per SM

@@ -228,7 +228,7 @@ __device__ __forceinline__ double unit_rates(const Prog<WP> &P, const uint4 &h, 
         d += 8;
     }
     const int ng = (int)(inf & 0xffu);
-#ifdef HQ_COMPACT
+#ifndef HQ_NO_COMPACT
 #pragma unroll 1
 #endif
     for (int g = 0; g < ng; g++) {
@@ -752,7 +752,7 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
             }
         }
         // ---- lane units 2..6 (lane bits 0..4): busy per lane
-#ifdef HQ_COMPACT   // one copy of the unit body (code size: the tile loop exceeds the instruction caches)
+#ifndef HQ_NO_COMPACT   // one copy of the unit body (code size: the tile loop exceeds the instruction caches)
 #pragma unroll 1
 #else
 #pragma unroll
@@ -801,7 +801,7 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
         // ---- tile units (H): two buffers, copied out before the refill two units ahead
         auto unit_H = [&](int h, double2 (&hb)[4]) {
             const int u = NVU + h;
-#ifdef HQ_H2   // consumed in place, refilled after use (no copy; one unit of latency cover)
+#if defined(HQ_H2) || defined(HQ_H4)   // consumed in place, refilled after use (no copy)
             double2 (&qq)[4] = hb;
 #else
             double2 qq[4];
@@ -819,7 +819,9 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
 #pragma unroll
                 for (int r = 0; r < R; r++) D[r] = fma(nuu, qv(qq, r), D[r]);
             }
-#ifdef HQ_H2
+#if defined(HQ_H4)
+            if (h + 4 < nH) hload(hsrc(h + 4), h + 4, hb);
+#elif defined(HQ_H2)
             if (h + 2 < nH) hload(hsrc(h + 2), h + 2, hb);
 #endif
         };
@@ -847,6 +849,22 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
 #pragma unroll
                 for (int r = 0; r < R; r++) D[r] = fma(nuu, qv(qq, r), D[r]);
             }
+        }
+#elif defined(HQ_H4)   // four slices in flight, each consumed in place and refilled four units ahead
+        double2 hb2[4], hb3[4];
+        if (nH > 2) hload(hsrc(2), 2, hb2);
+        if (nH > 3) hload(hsrc(3), 3, hb3);
+        for (int h = 0; h < nH; h += 4) {
+#pragma unroll
+            for (int hp = 0; hp < 4; hp += 2)
+                if (a.pf_h) {
+                    const int hh = h + hp + pf_hh;
+                    if (hh < nH && hh >= a.pf_min) prefetch_l2line(a.Q + ((jt ^ (1u << (T + hh))) | pf_lo));
+                }
+            unit_H(h, hb0);
+            if (h + 1 < nH) unit_H(h + 1, hb1);
+            if (h + 2 < nH) unit_H(h + 2, hb2);
+            if (h + 3 < nH) unit_H(h + 3, hb3);
         }
 #else
         for (int h = 0; h < nH; h += 2) {
