@@ -798,10 +798,12 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
             }
         }
 #ifndef HQ_HBUF3
-        // ---- tile units (H): two buffers, copied out before the refill two units ahead
+        // ---- tile units (H): two slice buffers, each consumed in place and refilled for the unit
+        // two ahead right after use (HQ_HCOPY: copied out first, refilled before use -- 16 register
+        // moves per unit and 16 more live registers; four in-place buffers spill: 2.3x slower)
         auto unit_H = [&](int h, double2 (&hb)[4]) {
             const int u = NVU + h;
-#if defined(HQ_H2) || defined(HQ_H4)   // consumed in place, refilled after use (no copy)
+#if !defined(HQ_HCOPY)   // consumed in place, refilled after use (no copy)
             double2 (&qq)[4] = hb;
 #else
             double2 qq[4];
@@ -819,9 +821,7 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
 #pragma unroll
                 for (int r = 0; r < R; r++) D[r] = fma(nuu, qv(qq, r), D[r]);
             }
-#if defined(HQ_H4)
-            if (h + 4 < nH) hload(hsrc(h + 4), h + 4, hb);
-#elif defined(HQ_H2)
+#if !defined(HQ_HCOPY)
             if (h + 2 < nH) hload(hsrc(h + 2), h + 2, hb);
 #endif
         };
@@ -849,22 +849,6 @@ __global__ void __launch_bounds__(512, 1) k_sweep3(S3Args a) {
 #pragma unroll
                 for (int r = 0; r < R; r++) D[r] = fma(nuu, qv(qq, r), D[r]);
             }
-        }
-#elif defined(HQ_H4)   // four slices in flight, each consumed in place and refilled four units ahead
-        double2 hb2[4], hb3[4];
-        if (nH > 2) hload(hsrc(2), 2, hb2);
-        if (nH > 3) hload(hsrc(3), 3, hb3);
-        for (int h = 0; h < nH; h += 4) {
-#pragma unroll
-            for (int hp = 0; hp < 4; hp += 2)
-                if (a.pf_h) {
-                    const int hh = h + hp + pf_hh;
-                    if (hh < nH && hh >= a.pf_min) prefetch_l2line(a.Q + ((jt ^ (1u << (T + hh))) | pf_lo));
-                }
-            unit_H(h, hb0);
-            if (h + 1 < nH) unit_H(h + 1, hb1);
-            if (h + 2 < nH) unit_H(h + 2, hb2);
-            if (h + 3 < nH) unit_H(h + 3, hb3);
         }
 #else
         for (int h = 0; h < nH; h += 2) {
@@ -2210,6 +2194,12 @@ static cudaError_t sweep_st(const S3Args &a, int full, int mode, int grid, cudaS
         if (full) return mode == 0 ? launch<0, true, WP, ST, WP ? 4 : 0>(a, grid, s) : launch<1, true, WP, ST, WP ? 4 : 0>(a, grid, s);
         return mode == 0 ? launch<0, false, WP, ST, WP ? 4 : 0>(a, grid, s) : launch<1, false, WP, ST, WP ? 4 : 0>(a, grid, s);
     }
+#ifdef HQ_NWC3   // development: 8-warp CTAs (HQ_NW=3, two CTAs per SM) with nW a compile-time constant
+    if (WP && a.nW == 3 && mode < 2) {
+        if (full) return mode == 0 ? launch<0, true, WP, ST, WP ? 3 : 0>(a, grid, s) : launch<1, true, WP, ST, WP ? 3 : 0>(a, grid, s);
+        return mode == 0 ? launch<0, false, WP, ST, WP ? 3 : 0>(a, grid, s) : launch<1, false, WP, ST, WP ? 3 : 0>(a, grid, s);
+    }
+#endif
 #endif
     if (full) {
         if (mode == 0) return launch<0, true, WP, ST>(a, grid, s);

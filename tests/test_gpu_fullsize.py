@@ -298,7 +298,7 @@ def test_group_lag_bitwise(hq, gb, lag):
     which order it sums them: pi and the measures are bitwise those of the unbounded run."""
     inst = hqinst.config_instance(4, N=23, J=200)
     base = {"HQ_ORDER": "group", "HQ_GROUP_BITS": str(gb)}
-    g0 = gpu_solve_env(hq, inst, base)
+    g0 = gpu_solve_env(hq, inst, dict(base, HQ_GLAG="0"))   # the default is lag 2 with >= 32 groups
     g1 = gpu_solve_env(hq, inst, dict(base, HQ_GLAG=str(lag)))
     assert g0["stats"]["group_lag"] == 0 and g1["stats"]["group_lag"] == lag
     assert g0["iters"] == g1["iters"] and g0["residual"] == g1["residual"]
