@@ -17,7 +17,9 @@
 //     staged in shared memory (double-buffered across tiles) with the tile's rate
 //     program by bulk copies (cp.async.bulk, the TMA engine) completed on an mbarrier,
 //   * tile bits ("H" units) come from the neighbour tiles' blocks in global memory
-//     (L2): coalesced 16-byte loads, two units ahead of the one accumulated.
+//     (L2): coalesced 16-byte loads into two register slice buffers, each consumed in
+//     place and refilled for the unit two ahead; the unit bodies are kept as loops (the
+//     tile loop must fit the SM's instruction caches: DESIGN.md §9).
 // The scatter weights (omega, kappa) and the old p (checks, residual) are read per
 // state in the epilogue.
 //
